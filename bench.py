@@ -1,0 +1,376 @@
+"""Benchmark: FGBD denoise of 1M-point frames on B200 (frames/s), driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one `denoise` of one 1M-point synthetic frame (BASELINE.json
+config 2: the paper's 30 fps case, `ramp` lattice k=100, b=7, Gaussian
+colour noise sigma=10, default FilterConfig; q saturates at 64 so S = 64
+filter steps, the heaviest LF load).
+
+value      device-resident throughput: inputs already in HBM, the C-ABI call
+           `fgbd_denoise(..., FGBD_FLAG_DEVICE_PTRS)`, CUDA events on the
+           library's stream, L2 flushed (256 MiB write) between steps and
+           excluded from the timed spans.  Whole job = N ranks x K frames /
+           max over ranks of the summed step time (frame-parallel, weak).
+e2e        the public API `paper_2401_09721_b200.denoise(PointCloud)` with
+           inputs in pinned host memory: H2D of coords+colours and D2H of the
+           denoised colours inside every timed step.
+roofline   dominant kernel k_lf_step (the random-walk step): SURVEY 8(d)
+           algorithmic bytes per step (52.125 N + 8 nnz) / its mean event-timed
+           duration, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the CPU oracle port (oracle/fgbd_oracle.py, numpy, the
+           reference's algorithm) on one frame of the same workload, rank 0, N=1.
+--impl reference  times that CPU port on all host cores (one process per
+           frame), same metric/config; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+KIND, N_POINTS, SIGMA = "ramp", 1_000_000, 10.0
+METRIC = "frames/sec at 1M pts/frame (FGBD denoise, 1 frame = 1 step)"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--kind", default=KIND)
+    ap.add_argument("--n", type=int, default=N_POINTS)
+    ap.add_argument("--sigma", type=float, default=SIGMA)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def make_frame(kind, n, sigma, seed):
+    import paper_2401_09721_b200 as fb
+
+    clean, _ = fb.generate_cloud(kind, n, seed=0)
+    return clean, fb.add_gaussian_noise(clean, sigma, seed=seed)
+
+
+def config_block(args, world, extra=None):
+    c = {"workload": f"single {args.n:,}-point synthetic '{args.kind}' frame, sigma={args.sigma:g}, "
+                     "default FilterConfig (BASELINE.json configs[1])",
+         "n_points": args.n, "kind": args.kind, "sigma": args.sigma,
+         "parallelism": f"frame-parallel x{world}" if world > 1 else "single GPU",
+         "l2": "flushed between timed steps (256 MiB write, untimed)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def run_b200(args):
+    import torch
+
+    import paper_2401_09721_b200 as fb
+    from paper_2401_09721_b200 import _native as nat
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    fb.use_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    clean, noisy = make_frame(args.kind, args.n, args.sigma, seed=1 + rank)
+    n = noisy.n_points
+    ctx = nat.context()
+    stream = torch.cuda.ExternalStream(ctx.lib.fgbd_ctx_stream(ctx.handle), device=local)
+    dev = torch.device("cuda", local)
+    d_coords = torch.from_numpy(np.ascontiguousarray(noisy.coords)).to(dev)
+    d_colors = torch.from_numpy(np.ascontiguousarray(noisy.colors)).to(dev)
+    d_out = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    cfg = nat.make_config(fb.FilterConfig())
+    torch.cuda.synchronize()
+
+    def step_device():
+        rep = nat.Report()
+        ctx.check(ctx.lib.fgbd_denoise(ctx.handle, d_coords.data_ptr(), d_colors.data_ptr(), n,
+                                       noisy.bit_depth, cfg, -1, float("nan"), d_out.data_ptr(),
+                                       rep, nat.FLAG_DEVICE_PTRS), "denoise")
+        return rep
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step_device()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    reps = []
+    with Clocks(local) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k)
+                ev[k][0].record(stream)
+            reps.append(step_device())
+            with torch.cuda.stream(stream):
+                ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    rep0 = reps[-1]
+    S = int(rep0.steps)
+    q = int(rep0.selected_q)
+    nnz = int(rep0.nnz)
+    # dominant kernel: the filter step, event-timed inside the library
+    lf_s = float(np.mean([r.t_lf_steps for r in reps])) / max(S, 1)
+    lf_bytes = 52.125 * n + 8.0 * nnz
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    tf = ROOT / "profiles" / "lf_step_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+    launches = int(sum(r.gpu_launches for r in reps))
+    stage = {"graph_construction_ms": 1e3 * float(np.mean([r.t_graph_construction for r in reps])),
+             "noise_estimation_ms": 1e3 * float(np.mean([r.t_noise_estimation for r in reps])),
+             "low_pass_filter_ms": 1e3 * float(np.mean([r.t_low_pass_filter for r in reps]))}
+    clocks = clk.summary()
+
+    # e2e: public API, pinned host inputs, H2D + D2H inside each step
+    e2e = None
+    if not args.no_e2e:
+        pc_coords = nat.pinned_empty(noisy.coords.shape, np.int64)
+        pc_coords[...] = noisy.coords
+        pc_colors = nat.pinned_empty(noisy.colors.shape, np.float64)
+        pc_colors[...] = noisy.colors
+        pc = fb.PointCloud(pc_coords, pc_colors, noisy.bit_depth)
+        assert pc.coords.ctypes.data == pc_coords.ctypes.data
+        for _ in range(2):
+            fb.denoise(pc)
+        barrier()
+        t_e2e = []
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out, rep = fb.denoise(pc)
+            t_e2e.append(time.perf_counter() - t0)
+        barrier()
+        e2e_s = float(sum(t_e2e))
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world * args.steps / e2e_s, "unit": "frames/s",
+               "h2d_bytes_per_step": int(pc.coords.nbytes + pc.colors.nbytes),
+               "d2h_bytes_per_step": int(out.colors.nbytes),
+               "ms_per_step": 1e3 * e2e_s / args.steps,
+               "path": "paper_2401_09721_b200.denoise(PointCloud) -> fgbd_denoise C-ABI, pinned host inputs"}
+
+    # CPU baseline + parity spot check (rank 0, N = 1 only)
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import fgbd_oracle as O
+
+        t0 = time.perf_counter()
+        ref = O.denoise(noisy.coords, noisy.colors, noisy.bit_depth)
+        t_cpu = time.perf_counter() - t0
+        cpu = {"value": 1.0 / t_cpu, "unit": "frames/s", "cores": 1, "kind": "port",
+               "sample": f"1 frame of the same workload ({n:,} pts, S={ref.steps}), "
+                         f"{t_cpu:.2f} s single-threaded numpy oracle"}
+        out_d = d_out.cpu().numpy()
+        parity = {"q_gpu": q, "q_ref": ref.selected_q, "S_gpu": S, "S_ref": ref.steps,
+                  "sigma_est_rel": abs(rep0.sigma_est - ref.sigma_est) / ref.sigma_est,
+                  "max_abs_color_diff": float(np.max(np.abs(out_d - ref.colors))),
+                  "psnr_gpu": fb.psnr(clean, noisy.with_colors(out_d)),
+                  "psnr_ref": fb.psnr(clean, noisy.with_colors(ref.colors))}
+        parity["dpsnr_db"] = parity["psnr_gpu"] - parity["psnr_ref"]
+
+    if rank == 0:
+        ms = total_ms / args.steps
+        line = {
+            "metric": METRIC, "value": world * args.steps / (total_ms / 1e3), "unit": "frames/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args, world, {"bit_depth": int(noisy.bit_depth),
+                                                 "selected_q": q, "filter_steps_S": S,
+                                                 "n_edges": int(rep0.n_edges)}),
+            "mpoints_per_s": world * args.steps * n / (total_ms / 1e3) / 1e6,
+            "stage_ms": stage,
+            "roofline": {"bound": "hbm", "kernel": "k_lf_step",
+                         "achieved": lf_bytes / lf_s / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": lf_bytes / lf_s / 1e9 / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": lf_bytes,
+                         "launch_ms": lf_s * 1e3, "peak_source": "MEASURED_PEAKS.json hbm_gbs"
+                         if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU port on all host cores
+# ---------------------------------------------------------------------------
+
+def _ref_worker(a):
+    kind, n, sigma, seed = a
+    sys.path.insert(0, str(ROOT))
+    from oracle import fgbd_oracle as O
+
+    _, noisy = make_frame(kind, n, sigma, seed)
+    t0 = time.perf_counter()
+    res = O.denoise(noisy.coords, noisy.colors, noisy.bit_depth)
+    return time.perf_counter() - t0, res.selected_q, res.steps
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2 ** 30
+    procs = max(1, min(cores, int(mem_gb // 3), 32))
+    env_thr = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS")}
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ctx = mp.get_context("spawn")
+    warm = min(args.warmup, 1)
+    walls, qs = [], set()
+    with ctx.Pool(procs) as pool:
+        for k in range(warm + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_ref_worker, [(args.kind, args.n, args.sigma, 1 + k * procs + i)
+                                         for i in range(procs)])
+            if k >= warm:
+                walls.append(time.perf_counter() - t0)
+                qs.update(r[1] for r in res)
+    total = float(sum(walls))
+    value = procs * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": warm, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_block(args, 1),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": procs, "kind": "port",
+                         "sample": f"each step = {procs} frames denoised concurrently, one "
+                                   f"single-threaded process per frame ({cores} cores visible, "
+                                   f"thread env {env_thr})"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "selected_q": sorted(qs),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

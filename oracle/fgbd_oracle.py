@@ -1,0 +1,545 @@
+"""CPU oracle for the FGBD denoise hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module is a numpy restatement of the reference algorithm
+(`/root/reference/pkg/src/fgbd/{graph,noise,filtering}.py`).  It exists to
+check the CUDA product path and to serve as the timed CPU baseline
+(`bench.py` cpu_baseline leg / `--impl reference`).  Only `tests/`,
+`__graft_entry__.smoke()` and `bench.py`'s CPU legs may import it; the
+product package `paper_2401_09721_b200` never does (it fails loudly when its
+CUDA library is missing instead of falling back here).
+
+Parity pinning: the outputs of this restatement are checked against golden
+vectors produced by running the unmodified reference in the build container
+(`tests/golden/make_golden.py`, fixtures under `tests/golden/`), and against
+the SPEC.md known-answer examples (`tests/test_oracle.py`).
+
+The restatement is deliberately *structurally different* from the reference
+where the reference's structure is an implementation accident:
+
+* the scan-line graph is built per point from rank neighbours (the shape the
+  GPU uses) instead of `np.unique` over packed pair keys, and the edge list /
+  `csr_edge` are derived as the row-major upper triangle -- the test suite
+  proves this equals the reference's lexicographic edge list;
+* the random-walk step is an ELL (padded rows) sequential accumulation
+  instead of a scipy CSR matvec; both accumulate `acc += w * f_j` in
+  ascending column order starting from 0.0 with no FMA, so they agree bit
+  for bit given the same weights.
+
+Everything operates on plain numpy arrays: coords (N, 3) int64, colors
+(N, 3) float64 in [0, 255].
+"""
+
+from __future__ import annotations
+
+import math
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# graph.py:25 -- (high, mid, low) coordinate axis of each scan-line code
+LINE_AXES = {1: (2, 1, 0), 2: (0, 2, 1), 3: (1, 0, 2)}
+
+JACOBI_MAX_SWEEPS = 50     # noise.py:21
+SYMMETRY_RTOL = 1e-9       # noise.py:22
+OFFDIAG_RTOL = 1e-12       # noise.py:23
+
+
+class OracleError(ValueError):
+    """Raised where the reference raises one of its ValueError subclasses."""
+
+    def __init__(self, kind: str, msg: str):
+        super().__init__(msg)
+        self.kind = kind  # "graph" | "noise" | "filter" | "all_excluded"
+
+
+# --------------------------------------------------------------------------
+# a2/a3: scan-line codes and the stable LSD radix argsort
+# --------------------------------------------------------------------------
+
+def scanline_codes(coords: np.ndarray, bit_depth: int, line: int) -> np.ndarray:
+    """Eqs. (1)-(3): code = hi << 2b | mid << b | lo  (graph.py:122-136)."""
+    hi, mid, lo = LINE_AXES[line]
+    g = np.asarray(coords).astype(np.uint64)
+    b = np.uint64(bit_depth)
+    return (g[:, hi] << (b + b)) | (g[:, mid] << b) | g[:, lo]
+
+
+def radix_argsort(keys: np.ndarray, key_bits: int = 64) -> np.ndarray:
+    """Stable LSD radix argsort, 8-bit digits, ceil(key_bits/8) passes.
+
+    Restates graph.py:139-171: each pass is a stable counting sort of the
+    current order by one byte of the key.  A stable numpy sort of the byte
+    column is exactly a stable counting pass.
+    """
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    n = keys.size
+    order = np.arange(n, dtype=np.int64)
+    if n < 2:
+        return order
+    for shift in range(0, key_bits, 8):
+        digit = (keys[order] >> np.uint64(shift)) & np.uint64(0xFF)
+        order = order[np.argsort(digit.astype(np.uint16), kind="stable")]
+    return order
+
+
+def sort_permutation(coords, bit_depth, line):
+    """graph.py:174-176."""
+    return radix_argsort(scanline_codes(coords, bit_depth, line), 3 * bit_depth)
+
+
+# --------------------------------------------------------------------------
+# a4/a5: scan-line graph in the reference's conventions
+# --------------------------------------------------------------------------
+
+@dataclass
+class OracleGraph:
+    n: int
+    indptr: np.ndarray      # (N+1,) int64
+    indices: np.ndarray     # (nnz,) int64, ascending within each row
+    csr_edge: np.ndarray    # (nnz,) int64 -> unique edge id
+    edge_u: np.ndarray      # (E,) int64, edge_u < edge_v, lexicographic
+    edge_v: np.ndarray
+    edge_sqdist: np.ndarray  # (E,) float64 (exact integers)
+    sigma_g: float | None = None
+    edge_weights: np.ndarray | None = None
+
+    @property
+    def n_edges(self):
+        return int(self.edge_u.size)
+
+    def degrees(self):
+        return np.diff(self.indptr)
+
+    def weighted_degrees(self):
+        """graph.py:78-85: bincount over edge_u plus bincount over edge_v.
+
+        Per vertex i that is (sum over j>i, ascending j) + (sum over j<i,
+        ascending j), each partial starting from 0.0.
+        """
+        w = self.edge_weights
+        return (np.bincount(self.edge_u, weights=w, minlength=self.n)
+                + np.bincount(self.edge_v, weights=w, minlength=self.n))
+
+    def csr_weights(self):
+        return self.edge_weights[self.csr_edge]
+
+
+def _rows_from_candidates(cand: np.ndarray, n: int):
+    """Sort + dedup up to 6 candidate neighbours per point (-1 = none)."""
+    big = np.int64(n)  # sentinel sorts after every real index
+    c = np.where(cand < 0, big, cand)
+    c.sort(axis=1)
+    dup = np.zeros_like(c, dtype=bool)
+    dup[:, 1:] = c[:, 1:] == c[:, :-1]
+    c[dup] = big
+    c.sort(axis=1)
+    valid = c < big
+    deg = valid.sum(axis=1)
+    indptr = np.zeros(n + 1, np.int64)
+    np.cumsum(deg, out=indptr[1:])
+    return indptr, c[valid].astype(np.int64)
+
+
+def build_slg(coords: np.ndarray, bit_depth: int) -> OracleGraph:
+    """Scan-line graph (graph.py:179-224), built per point.
+
+    Under scan line l, point perm_l[k] is adjacent to perm_l[k-1] and
+    perm_l[k+1].  The union over l=1..3 with duplicates removed, rows sorted
+    by index, is exactly the reference's CSR; unique edges are the upper
+    triangle (j > i) enumerated row-major, which is the lexicographic order
+    `np.unique(lo * n + hi)` produces.
+    """
+    coords = np.asarray(coords, np.int64)
+    n = coords.shape[0]
+    if n >= 2 ** 31:
+        raise OracleError("graph", "point count exceeds the 2^31 edge-encoding limit")
+    if n < 2:
+        e = np.empty(0, np.int64)
+        return OracleGraph(n, np.zeros(n + 1, np.int64), e, e, e, e, np.empty(0))
+    cand = np.full((n, 6), -1, np.int64)
+    for li, line in enumerate((1, 2, 3)):
+        perm = sort_permutation(coords, bit_depth, line)
+        cand[perm[1:], 2 * li] = perm[:-1]     # predecessor on the scan line
+        cand[perm[:-1], 2 * li + 1] = perm[1:]  # successor on the scan line
+    indptr, indices = _rows_from_candidates(cand, n)
+    row = np.repeat(np.arange(n, dtype=np.int64), np.diff(indptr))
+    upper = indices > row
+    edge_u = row[upper]
+    edge_v = indices[upper]
+    # edge id of every slot: upper slots are numbered in order; a lower slot
+    # (i, j<i) is edge (j, i), found by binary search in the sorted key list.
+    ukey = edge_u * n + edge_v
+    skey = np.where(upper, row * n + indices, indices * n + row)
+    csr_edge = np.searchsorted(ukey, skey).astype(np.int64)
+    d = (coords[edge_u] - coords[edge_v]).astype(np.float64)
+    sqdist = d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1] + d[:, 2] * d[:, 2]
+    return OracleGraph(n, indptr, indices, csr_edge, edge_u, edge_v, sqdist)
+
+
+def compute_sigma_g(g: OracleGraph) -> float:
+    """graph.py:227-233: mean Euclidean length of the unique edges."""
+    if g.n_edges == 0:
+        raise OracleError("graph", "cannot compute a distance scale on an edgeless graph")
+    return float(np.mean(np.sqrt(g.edge_sqdist)))
+
+
+def apply_gaussian_weights(g: OracleGraph, sigma_g: float) -> OracleGraph:
+    """Eq. (4), graph.py:236-245: w = exp(-sqdist / sigma_g^2)."""
+    if not sigma_g > 0:
+        raise OracleError("graph", f"sigma_g must be positive, got {sigma_g}")
+    g.sigma_g = float(sigma_g)
+    g.edge_weights = np.exp(-g.edge_sqdist / float(sigma_g) ** 2)
+    return g
+
+
+def build_weighted_slg(coords, bit_depth) -> OracleGraph:
+    g = build_slg(coords, bit_depth)
+    return apply_gaussian_weights(g, compute_sigma_g(g))
+
+
+# --------------------------------------------------------------------------
+# a9-a13: NE-GBP
+# --------------------------------------------------------------------------
+
+def extract_patches(colors: np.ndarray, g: OracleGraph, patch_size: int):
+    """noise.py:82-119.  Returns (vectors (3, ne, D), eligible point ids).
+
+    Patch = own value, then the D-1 nearest graph neighbours ordered by
+    (squared distance, index).
+    """
+    d = int(patch_size)
+    if d < 2:
+        raise OracleError("noise", f"patch_size must be >= 2, got {patch_size}")
+    deg = g.degrees()
+    max_deg = int(deg.max(initial=0))
+    if d > 1 + max_deg:
+        raise OracleError("noise", f"patch_size {d} exceeds 1 + max degree ({1 + max_deg}) of this graph")
+    elig = np.flatnonzero(deg >= d - 1)
+    ne = elig.size
+    width = max(max_deg, 1)
+    col = np.arange(width)[None, :]
+    ln = deg[elig][:, None]
+    ok = col < ln
+    pos = g.indptr[elig][:, None] + np.minimum(col, np.maximum(ln - 1, 0))
+    nbr = np.where(ok, g.indices[pos] if g.indices.size else 0, np.int64(g.n))
+    slot_d = g.edge_sqdist[g.csr_edge] if g.csr_edge.size else np.empty(0)
+    dist = np.where(ok, slot_d[pos] if slot_d.size else 0.0, np.inf)
+    order = np.lexsort((nbr, dist), axis=1)[:, : d - 1]
+    pick = np.take_along_axis(nbr, order, axis=1)
+    vec = np.empty((3, ne, d))
+    for c in range(3):
+        vec[c, :, 0] = colors[elig, c]
+        vec[c, :, 1:] = colors[:, c][pick]
+    return vec, elig
+
+
+def patch_covariance(x: np.ndarray) -> np.ndarray:
+    """noise.py:122-130: population covariance of one channel's (ne, D) patches."""
+    ne = x.shape[0]
+    if ne < 2:
+        raise OracleError("noise", f"need at least 2 patches, have {ne}")
+    xc = x - x.mean(axis=0)
+    s = (xc.T @ xc) / ne
+    return (s + s.T) * 0.5
+
+
+def symmetric_eigenvalues(s: np.ndarray, max_sweeps: int = JACOBI_MAX_SWEEPS) -> np.ndarray:
+    """Cyclic Jacobi, descending eigenvalues (noise.py:133-185).
+
+    Rotation (p<q): t from theta = (a_qq - a_pp) / (2 a_pq),
+    c = 1/sqrt(1+t^2), s = t c; columns then rows are rotated and a_pq is
+    zeroed.  Converged when the off-diagonal Frobenius norm <= 1e-12 ||S||.
+    """
+    s = np.asarray(s, np.float64)
+    if s.ndim != 2 or s.shape[0] != s.shape[1]:
+        raise OracleError("noise", f"matrix must be square, got {s.shape}")
+    scale = np.abs(s).max()
+    if scale > 0 and np.abs(s - s.T).max() > SYMMETRY_RTOL * scale:
+        raise OracleError("noise", "matrix is not symmetric within tolerance")
+    a = np.array((s + s.T) * 0.5)
+    n = a.shape[0]
+    fro = np.linalg.norm(a)
+    if fro == 0.0 or n == 1:
+        return np.sort(np.diag(a))[::-1]
+    tol = OFFDIAG_RTOL * fro
+
+    def off_norm():
+        return math.sqrt(max(float(np.sum(a * a) - np.sum(np.diag(a) ** 2)), 0.0))
+
+    for _ in range(max_sweeps):
+        if off_norm() <= tol:
+            return np.sort(np.diag(a))[::-1]
+        for p in range(n - 1):
+            for q in range(p + 1, n):
+                apq = a[p, q]
+                if apq == 0.0:
+                    continue
+                gap = a[q, q] - a[p, p]
+                if abs(apq) < 1e-36 * abs(gap):
+                    t = apq / gap
+                else:
+                    th = gap / (2.0 * apq)
+                    t = np.sign(th) / (abs(th) + np.hypot(th, 1.0))
+                    if t == 0.0:
+                        t = 1.0
+                c = 1.0 / np.sqrt(t * t + 1.0)
+                sn = t * c
+                cp, cq = a[:, p].copy(), a[:, q].copy()
+                a[:, p] = c * cp - sn * cq
+                a[:, q] = sn * cp + c * cq
+                rp, rq = a[p, :].copy(), a[q, :].copy()
+                a[p, :] = c * rp - sn * rq
+                a[q, :] = sn * rp + c * rq
+                a[p, q] = a[q, p] = 0.0
+    if off_norm() <= tol:
+        return np.sort(np.diag(a))[::-1]
+    raise OracleError("noise", f"Jacobi did not converge in {max_sweeps} sweeps")
+
+
+def select_tail(lam: np.ndarray, divisor: str = "count"):
+    """noise.py:188-216 -> (m, tau, fallback)."""
+    lam = np.asarray(lam, np.float64)
+    d = lam.size
+    if d < 3:
+        raise OracleError("noise", f"need at least 3 eigenvalues, got {d}")
+    if divisor not in ("count", "count_plus_one"):
+        raise OracleError("noise", f"unknown divisor rule {divisor!r}")
+    extra = 0 if divisor == "count" else 1
+    for m in range(1, d - 1):
+        tail = lam[m:]
+        tau = float(tail.sum() / (tail.size + extra))
+        if tau > float(np.median(tail)):
+            return m, tau, False
+    m = d // 2
+    tail = lam[m:]
+    return m, float(tail.sum() / (tail.size + extra)), True
+
+
+@dataclass
+class OracleNoise:
+    sigma_est: float
+    per_channel_sigma: np.ndarray
+    eigenvalues: np.ndarray
+    m: np.ndarray
+    tau: np.ndarray
+    fallback: np.ndarray
+    eligible_count: int
+
+
+def estimate_noise_from_patches(vec: np.ndarray, divisor: str = "count") -> OracleNoise:
+    """noise.py:219-243."""
+    d = vec.shape[2]
+    lam = np.empty((3, d))
+    m = np.empty(3, np.int64)
+    tau = np.empty(3)
+    fb = np.empty(3, bool)
+    sig = np.empty(3)
+    for c in range(3):
+        lam[c] = symmetric_eigenvalues(patch_covariance(vec[c]))
+        m[c], tau[c], fb[c] = select_tail(lam[c], divisor)
+        sig[c] = math.sqrt(max(tau[c], 0.0))
+    return OracleNoise(float(sig.mean()), sig, lam, m, tau, fb, int(vec.shape[1]))
+
+
+# --------------------------------------------------------------------------
+# a14: FSLR
+# --------------------------------------------------------------------------
+
+def fslr_stat(vec: np.ndarray) -> np.ndarray:
+    """Mean over channels of the population std of each patch (filtering.py:186)."""
+    return vec.std(axis=2).mean(axis=0)
+
+
+def fslr_mask(vec, elig, n, sigma_est, sigma_floor=0.5) -> np.ndarray:
+    """filtering.py:175-194 -> include (N,) bool.  Raises all_excluded."""
+    if sigma_est < sigma_floor:
+        return np.ones(n, bool)
+    inc = np.ones(n, bool)
+    inc[elig[fslr_stat(vec) > 2.0 * sigma_est]] = False
+    if not inc.any():
+        raise OracleError("all_excluded", "the variance threshold excluded every point")
+    return inc
+
+
+# --------------------------------------------------------------------------
+# a15-a18: random-walk low-pass filter and q selection
+# --------------------------------------------------------------------------
+
+class EllOperator:
+    """Padded-row view of the weighted graph for the matvec.
+
+    Row i holds its neighbours in ascending column order followed by
+    (index 0, weight 0.0) padding.  Accumulating `acc = acc + w * f_j` over
+    the padded columns from acc = 0.0 reproduces scipy's csr_matvecs
+    (`y[i] += a * x[j]` in slot order) exactly: adding a +0.0 product does
+    not change a finite accumulator.
+    """
+
+    def __init__(self, g: OracleGraph):
+        deg = g.degrees()
+        width = int(deg.max(initial=0))
+        n = g.n
+        self.width = width
+        self.idx = np.zeros((n, max(width, 1)), np.int64)
+        self.w = np.zeros((n, max(width, 1)), np.float64)
+        if width:
+            col = np.arange(width)[None, :]
+            ok = col < deg[:, None]
+            pos = (g.indptr[:-1][:, None] + col)[ok]
+            self.idx[ok] = g.indices[pos]
+            self.w[ok] = g.csr_weights()[pos]
+        self.d = g.weighted_degrees()
+
+    def step(self, f: np.ndarray) -> np.ndarray:
+        """filtering.py:132-155: out = (d f + W f) / (2 d); d == 0 passes through."""
+        acc = np.zeros_like(f)
+        for s in range(self.width):
+            acc = acc + self.w[:, s, None] * f[self.idx[:, s]]
+        dcol = self.d[:, None]
+        with np.errstate(invalid="ignore", divide="ignore"):
+            out = (dcol * f + acc) / (2.0 * dcol)
+        iso = self.d == 0.0
+        if iso.any():
+            out[iso] = f[iso]
+        return out
+
+
+def selection_criterion(y, x, include, sigma_est, mode="pooled") -> float:
+    """Eq. (6), filtering.py:197-222."""
+    count = int(include.sum())
+    if count < 1:
+        raise OracleError("filter", "criterion needs at least one included point")
+    sv2 = float(sigma_est) ** 2
+    if mode == "pooled":
+        lost = (np.sum(y[include] ** 2) - np.sum(x[include] ** 2)) / (count * y.shape[1])
+        return float(abs(sv2 - lost))
+    if mode == "per_channel":
+        lost = (np.sum(y[include] ** 2, axis=0) - np.sum(x[include] ** 2, axis=0)) / count
+        return float(np.mean(np.abs(sv2 - lost)))
+    raise OracleError("filter", f"unknown criterion mode {mode!r}")
+
+
+def select_q(y, op: EllOperator, sigma_est, include, q_max=64, mode="pooled",
+             early_exit=True, trace=None):
+    """filtering.py:225-256.  Returns (q, x_q, steps_executed).
+
+    `trace`, when a list, receives the criterion value of every q visited.
+    """
+    if sigma_est < 0:
+        raise OracleError("filter", f"sigma_est must be >= 0, got {sigma_est}")
+    x = y.copy()
+    best_q, best_x = 0, x.copy()
+    best = selection_criterion(y, x, include, sigma_est, mode)
+    if trace is not None:
+        trace.append(best)
+    prev, streak, steps = best, 0, 0
+    for q in range(1, q_max + 1):
+        if best == 0.0:
+            break
+        x = op.step(x)
+        steps += 1
+        crit = selection_criterion(y, x, include, sigma_est, mode)
+        if trace is not None:
+            trace.append(crit)
+        if crit < best:
+            best_q, best, best_x = q, crit, x.copy()
+        streak = streak + 1 if crit > prev else 0
+        prev = crit
+        if early_exit and streak >= 3:
+            break
+    return best_q, best_x, steps
+
+
+@dataclass
+class OracleConfig:
+    """Mirror of FilterConfig (filtering.py:33-59)."""
+    q_max: int = 64
+    epsilon: float | None = None
+    fslr_enabled: bool = True
+    patch_size: int = 7
+    reestimate_interval: int = 10
+    fslr_sigma_floor: float = 0.5
+    criterion_mode: str = "pooled"
+    early_exit: bool = True
+    tau_divisor: str = "count"
+
+
+@dataclass
+class OracleResult:
+    colors: np.ndarray
+    selected_q: int
+    sigma_est: float
+    masked_fraction: float
+    criterion_value: float | None = None
+    converged: bool | None = None
+    cached: bool = False
+    eligible_count: int | None = None
+    steps: int = 0
+    all_excluded_fallback: bool = False
+    noise: OracleNoise | None = None
+    include: np.ndarray | None = None
+    graph: OracleGraph | None = None
+    trace: list = field(default_factory=list)
+    stage_timings: dict = field(default_factory=dict)
+
+
+def denoise(coords, colors, bit_depth, cfg: OracleConfig | None = None,
+            cached_q: int | None = None, cached_sigma_est: float | None = None,
+            keep_graph: bool = False) -> OracleResult:
+    """filtering.py:259-328 on plain arrays."""
+    cfg = cfg or OracleConfig()
+    coords = np.asarray(coords, np.int64)
+    y = np.asarray(colors, np.float64)
+    n = coords.shape[0]
+    if n < 2:
+        return OracleResult(y, 0, 0.0, 0.0)
+    t = {}
+    t0 = time.perf_counter()
+    g = build_weighted_slg(coords, bit_depth)
+    op = EllOperator(g)
+    t["graph_construction"] = time.perf_counter() - t0
+    if cached_q is None:
+        t0 = time.perf_counter()
+        vec, elig = extract_patches(y, g, cfg.patch_size)
+        est = estimate_noise_from_patches(vec, cfg.tau_divisor)
+        fallback = False
+        if cfg.fslr_enabled:
+            try:
+                inc = fslr_mask(vec, elig, n, est.sigma_est, cfg.fslr_sigma_floor)
+            except OracleError as e:
+                if e.kind != "all_excluded":
+                    raise
+                warnings.warn("variance mask excluded every point; selecting unmasked")
+                inc = np.ones(n, bool)
+                fallback = True
+        else:
+            inc = np.ones(n, bool)
+        t["noise_estimation"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        trace: list = []
+        q, x, steps = select_q(y, op, est.sigma_est, inc, cfg.q_max,
+                               cfg.criterion_mode, cfg.early_exit, trace)
+        t["low_pass_filter"] = time.perf_counter() - t0
+        crit = selection_criterion(y, x, inc, est.sigma_est, cfg.criterion_mode)
+        eps = cfg.epsilon if cfg.epsilon is not None else 1e-3 * est.sigma_est ** 2
+        res = OracleResult(np.clip(x, 0.0, 255.0), q, est.sigma_est,
+                           1.0 - int(inc.sum()) / n, crit, bool(crit <= eps), False,
+                           est.eligible_count, steps, fallback, est, inc,
+                           trace=trace, stage_timings=t)
+    else:
+        if cached_q < 0:
+            raise OracleError("filter", f"cached_q must be >= 0, got {cached_q}")
+        t["noise_estimation"] = 0.0
+        t0 = time.perf_counter()
+        x = y
+        for _ in range(cached_q):
+            x = op.step(x)
+        t["low_pass_filter"] = time.perf_counter() - t0
+        res = OracleResult(np.clip(x, 0.0, 255.0), int(cached_q),
+                           float(cached_sigma_est) if cached_sigma_est is not None else 0.0,
+                           0.0, cached=True, steps=int(cached_q), stage_timings=t)
+    if keep_graph:
+        res.graph = g
+    return res

@@ -1,0 +1,73 @@
+"""Build the in-tree CUDA library `_lib/libfgbd_b200.so` for sm_100a.
+
+Plain nvcc, no torch extension machinery: the product is a C-ABI shared
+library (include/fgbd_b200.h) with the CUDA runtime linked statically, so
+it loads next to any torch build.  Objects are rebuilt only when a source
+or header is newer than them.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+INCLUDE = ROOT / "include"
+OUT_DIR = PKG / "_lib"
+LIB = OUT_DIR / "libfgbd_b200.so"
+SOURCES = ["graph.cu", "noise.cu", "filter.cu", "stage.cu", "api.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+              "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found; the B200 library cannot be built")
+
+
+def _headers():
+    return list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
+
+
+def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> Path:
+    nvcc = _nvcc()
+    OUT_DIR.mkdir(exist_ok=True)
+    obj_dir = ROOT / "build" / "obj"
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    hdr_mtime = max((h.stat().st_mtime for h in _headers()), default=0)
+    objs = []
+    rebuilt = False
+    for src in SOURCES:
+        s = CSRC / src
+        o = obj_dir / (s.stem + ".o")
+        objs.append(o)
+        if not force and o.exists() and o.stat().st_mtime >= max(s.stat().st_mtime, hdr_mtime):
+            continue
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(s), "-o", str(o)]
+        if ptxas_v:
+            cmd[1:1] = ["-Xptxas", "-v"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        rebuilt = True
+    if rebuilt or force or not LIB.exists():
+        tmp = LIB.with_suffix(".so.tmp")
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-cudart", "static"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose=True, force="--force" in sys.argv, ptxas_v="-v" in sys.argv)
+    print(LIB)

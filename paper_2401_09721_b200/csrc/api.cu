@@ -1,0 +1,812 @@
+// C ABI (include/fgbd_b200.h): context lifetime, the `denoise` drop-in
+// (reference filtering.py:259-328) and the stage entry points.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fgbd_internal.cuh"
+
+namespace fgbd {
+
+thread_local std::string g_global_err;
+
+int set_error(fgbd_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  else g_global_err = msg;
+  return code;
+}
+
+int cuda_error(fgbd_ctx* ctx, cudaError_t e, const char* where) {
+  return set_error(ctx, FGBD_E_CUDA,
+                   std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+static int dalloc(fgbd_ctx* ctx, T** p, size_t count) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  if (count == 0) count = 1;
+  const size_t bytes = count * sizeof(T);
+  FGBD_CUDA(ctx, cudaMalloc((void**)p, bytes));
+  ctx->dev_bytes += bytes;
+  return FGBD_OK;
+}
+
+static void free_scratch(fgbd_ctx* ctx) {
+  auto f = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  f(ctx->coords64);
+  f(ctx->pc);
+  for (int a = 0; a < 2; ++a)
+    for (int l = 0; l < 3; ++l) {
+      f(ctx->sort.keys[a][l]);
+      f(ctx->sort.vals[a][l]);
+      ctx->sort.keys[a][l] = nullptr;
+      ctx->sort.vals[a][l] = nullptr;
+    }
+  f(ctx->sort.status);
+  f(ctx->cand);
+  f(ctx->ell);
+  f(ctx->w64);
+  f(ctx->meta);
+  for (int k = 0; k < 3; ++k) {
+    f(ctx->buf[k]);
+    ctx->buf[k] = nullptr;
+  }
+  f(ctx->out);
+  f(ctx->fslr);
+  f(ctx->mask);
+  ctx->coords64 = nullptr;
+  ctx->pc = nullptr;
+  ctx->sort.status = nullptr;
+  ctx->cand = nullptr;
+  ctx->ell = nullptr;
+  ctx->w64 = nullptr;
+  ctx->meta = nullptr;
+  ctx->out = nullptr;
+  ctx->fslr = nullptr;
+  ctx->mask = nullptr;
+  ctx->cap = 0;
+  ctx->dev_bytes = 0;
+  ctx->g_n = -1;
+}
+
+int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64) {
+  if (n <= ctx->cap && (!key64 || ctx->key64_cap)) return FGBD_OK;
+  int64_t cap = std::max<int64_t>(n, ctx->cap);
+  cap = ((cap + 65535) / 65536) * 65536;
+  const int k64 = key64 || ctx->key64_cap;
+  free_scratch(ctx);
+  const size_t ksz = k64 ? 8 : 4;
+  int rc;
+  if ((rc = dalloc(ctx, &ctx->coords64, 3 * cap))) return rc;
+  if ((rc = dalloc(ctx, (unsigned long long**)&ctx->pc, cap))) return rc;
+  for (int a = 0; a < 2; ++a)
+    for (int l = 0; l < 3; ++l) {
+      if ((rc = dalloc(ctx, (unsigned char**)&ctx->sort.keys[a][l], cap * ksz))) return rc;
+      if ((rc = dalloc(ctx, &ctx->sort.vals[a][l], cap))) return rc;
+    }
+  const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
+  if ((rc = dalloc(ctx, &ctx->sort.status, 3 * tiles * kRadix))) return rc;
+  FGBD_CUDA(ctx, cudaMemset(ctx->sort.status, 0, 3 * tiles * kRadix * 8));
+  ctx->sort.tiles_cap = tiles;
+  if ((rc = dalloc(ctx, &ctx->cand, 3 * cap))) return rc;
+  if ((rc = dalloc(ctx, &ctx->ell, kSlots * cap))) return rc;
+  if ((rc = dalloc(ctx, &ctx->meta, cap))) return rc;
+  for (int k = 0; k < 3; ++k)
+    if ((rc = dalloc(ctx, &ctx->buf[k], 3 * cap))) return rc;
+  if ((rc = dalloc(ctx, &ctx->out, 3 * cap))) return rc;
+  if ((rc = dalloc(ctx, &ctx->fslr, cap))) return rc;
+  if ((rc = dalloc(ctx, &ctx->mask, (cap + 31) / 32 + 1))) return rc;
+  FGBD_CUDA(ctx, cudaMemcpy(ctx->d_bufs, ctx->buf, sizeof(ctx->buf), cudaMemcpyHostToDevice));
+  ctx->cap = cap;
+  ctx->key64_cap = k64;
+  return FGBD_OK;
+}
+
+int ensure_w64(fgbd_ctx* ctx, int64_t n) {
+  if (ctx->w64) return FGBD_OK;
+  return dalloc(ctx, &ctx->w64, kSlots * ctx->cap);
+}
+
+}  // namespace fgbd
+
+using namespace fgbd;
+
+namespace {
+
+int check_cfg(fgbd_ctx* ctx, const fgbd_config* c) {
+  if (!c) return set_error(ctx, FGBD_E_ARG, "config must not be NULL");
+  if (c->q_max < 0)
+    return set_error(ctx, FGBD_E_FILTER, "q_max must be >= 0, got " + std::to_string(c->q_max));
+  if (c->reestimate_interval < 1)
+    return set_error(ctx, FGBD_E_FILTER, "reestimate_interval must be >= 1, got " +
+                                             std::to_string(c->reestimate_interval));
+  if (c->patch_size < 2)
+    return set_error(ctx, FGBD_E_FILTER,
+                     "patch_size must be >= 2, got " + std::to_string(c->patch_size));
+  if (c->criterion_mode != FGBD_CRIT_POOLED && c->criterion_mode != FGBD_CRIT_PER_CHANNEL)
+    return set_error(ctx, FGBD_E_FILTER, "unknown criterion_mode");
+  if (c->tau_divisor != FGBD_TAU_COUNT && c->tau_divisor != FGBD_TAU_COUNT_PLUS_ONE)
+    return set_error(ctx, FGBD_E_NOISE, "unknown divisor rule");
+  return FGBD_OK;
+}
+
+int check_graph_input(fgbd_ctx* ctx, int64_t n, int bits) {
+  if (bits < 1 || bits > 21)
+    return set_error(ctx, FGBD_E_GRAPH, "bit depth " + std::to_string(bits) +
+                                            " exceeds 21 (64-bit code overflow)");
+  if (n >= (int64_t(1) << 31))
+    return set_error(ctx, FGBD_E_GRAPH, "point count exceeds the 2^31 edge-encoding limit");
+  return FGBD_OK;
+}
+
+int h2d(fgbd_ctx* ctx, void* dst, const void* src, size_t bytes, bool dev) {
+  if (bytes == 0) return FGBD_OK;
+  FGBD_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes,
+                                 dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 ctx->stream));
+  return FGBD_OK;
+}
+
+int d2h(fgbd_ctx* ctx, void* dst, const void* src, size_t bytes, bool dev) {
+  if (bytes == 0) return FGBD_OK;
+  FGBD_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes,
+                                 dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  return FGBD_OK;
+}
+
+int pull_ctl(fgbd_ctx* ctx) {
+  FGBD_CUDA(ctx, cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FGBD_OK;
+}
+
+int reset_ctl(fgbd_ctx* ctx) {
+  FGBD_CUDA(ctx, cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
+  return FGBD_OK;
+}
+
+// Load a frame's coordinates and build the weighted scan-line graph.
+int stage_graph(fgbd_ctx* ctx, const int64_t* coords, int64_t n, int bits, bool dev, int w64) {
+  int rc = ensure_capacity(ctx, n, 3 * bits > 32);
+  if (rc) return rc;
+  if ((rc = reset_ctl(ctx))) return rc;
+  if (dev) {
+    ctx->cur_coords = coords;
+  } else {
+    if ((rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false))) return rc;
+    ctx->cur_coords = ctx->coords64;
+  }
+  if ((rc = launch_graph(ctx, n, bits))) return rc;
+  return launch_weights(ctx, n, bits, w64);
+}
+
+int check_graph_ctl(fgbd_ctx* ctx, int bits) {
+  const Ctl& h = *ctx->ctl_host;
+  if (h.err_flags & 1)
+    return set_error(ctx, FGBD_E_CLOUD,
+                     "coordinates out of range for bit_depth=" + std::to_string(bits));
+  if (!(h.sigma_g > 0)) {
+    char b[96];
+    std::snprintf(b, sizeof(b), "sigma_g must be positive, got %.17g", h.sigma_g);
+    return set_error(ctx, FGBD_E_GRAPH, b);
+  }
+  return FGBD_OK;
+}
+
+double ev_sec(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.0;
+  }
+  return ms * 1e-3;
+}
+
+void fill_noise_report(fgbd_report* r, const fgbd_noise& nz) {
+  for (int c = 0; c < 3; ++c) {
+    r->per_channel_sigma[c] = nz.per_channel_sigma[c];
+    r->tail_m[c] = nz.m[c];
+    r->tail_tau[c] = nz.tau[c];
+    r->tail_fallback[c] = nz.fallback[c];
+    for (int k = 0; k < FGBD_MAX_PATCH; ++k) r->eigenvalues[c][k] = nz.eigenvalues[c][k];
+  }
+  r->eligible_count = nz.eligible_count;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t fgbd_abi_version(void) { return FGBD_ABI_VERSION; }
+
+const char* fgbd_last_error(const fgbd_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_global_err.c_str();
+}
+
+fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_error(nullptr, FGBD_E_CUDA, std::string("no CUDA device available: ") +
+                                        (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+    return nullptr;
+  }
+  if (device < 0 || device >= ndev) {
+    set_error(nullptr, FGBD_E_ARG, "device index out of range");
+    return nullptr;
+  }
+  fgbd_ctx* ctx = new fgbd_ctx();
+  ctx->device = device;
+  auto fail = [&](cudaError_t err, const char* w) -> fgbd_ctx* {
+    set_error(nullptr, FGBD_E_CUDA, std::string(w) + ": " + cudaGetErrorString(err));
+    delete ctx;
+    return nullptr;
+  };
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return fail(e, "cudaSetDevice");
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return fail(e, "props");
+  if (prop.major < 10) {
+    set_error(nullptr, FGBD_E_CUDA, "device is not sm_100 (Blackwell); this build targets sm_100a");
+    delete ctx;
+    return nullptr;
+  }
+  ctx->num_sms = prop.multiProcessorCount;
+  if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(e, "stream");
+  for (auto& ev : ctx->ev)
+    if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(e, "event");
+  if ((e = cudaMalloc(&ctx->ctl, sizeof(Ctl))) != cudaSuccess) return fail(e, "ctl");
+  if ((e = cudaMemset(ctx->ctl, 0, sizeof(Ctl))) != cudaSuccess) return fail(e, "ctl");
+  if ((e = cudaMallocHost(&ctx->ctl_host, sizeof(Ctl))) != cudaSuccess) return fail(e, "ctl host");
+  if ((e = cudaMalloc(&ctx->partials, (1 << 17) * sizeof(double))) != cudaSuccess)
+    return fail(e, "partials");
+  if ((e = cudaMalloc(&ctx->sort.hist, 3 * kMaxPasses * kRadix * sizeof(uint32_t))) != cudaSuccess)
+    return fail(e, "hist");
+  if ((e = cudaMalloc(&ctx->sort.tile_ctr, 3 * kMaxPasses * sizeof(unsigned))) != cudaSuccess)
+    return fail(e, "tile ctr");
+  if ((e = cudaMalloc(&ctx->d_bufs, 3 * sizeof(double*))) != cudaSuccess) return fail(e, "bufs");
+  if (max_points > 0 && ensure_capacity(ctx, max_points, 0) != FGBD_OK) {
+    set_error(nullptr, FGBD_E_CUDA, ctx->err);
+    fgbd_ctx_destroy(ctx);
+    return nullptr;
+  }
+  return ctx;
+}
+
+void fgbd_ctx_destroy(fgbd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  free_scratch(ctx);
+  if (ctx->ctl) cudaFree(ctx->ctl);
+  if (ctx->ctl_host) cudaFreeHost(ctx->ctl_host);
+  if (ctx->partials) cudaFree(ctx->partials);
+  if (ctx->sort.hist) cudaFree(ctx->sort.hist);
+  if (ctx->sort.tile_ctr) cudaFree(ctx->sort.tile_ctr);
+  if (ctx->d_bufs) cudaFree(ctx->d_bufs);
+  if (ctx->csr_scratch) cudaFree(ctx->csr_scratch);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+void* fgbd_ctx_stream(fgbd_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int64_t fgbd_ctx_device_bytes(const fgbd_ctx* ctx) { return ctx ? (int64_t)ctx->dev_bytes : 0; }
+
+void* fgbd_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, (size_t)bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void fgbd_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors, int64_t n,
+                     int32_t bits, const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
+                     double* out_colors, fgbd_report* rep, uint32_t flags) {
+  if (!ctx || !rep) return set_error(ctx, FGBD_E_ARG, "null context or report");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  ctx->launches = 0;
+  int rc = check_cfg(ctx, cfg);
+  if (rc) return rc;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->criterion_value = NAN;
+  rep->converged = -1;
+  rep->eligible_count = -1;
+  if (n < 0) return set_error(ctx, FGBD_E_ARG, "n must be >= 0");
+  const bool dev = (flags & FGBD_FLAG_DEVICE_PTRS) != 0;
+  const bool timing = !(flags & FGBD_FLAG_NO_TIMING);
+  const int w64 = (flags & FGBD_FLAG_WEIGHTS_F64) ? 1 : 0;
+  if (n < 2) {  // filtering.py:269-275: the input comes back unchanged
+    if (n > 0 && out_colors != colors) {
+      if ((rc = d2h(ctx, out_colors, colors, 3 * n * sizeof(double), dev))) return rc;
+      FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return FGBD_OK;
+  }
+  if ((rc = check_graph_input(ctx, n, bits))) return rc;
+  cudaEvent_t* ev = ctx->ev;
+  if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
+  if ((rc = ensure_capacity(ctx, n, 3 * bits > 32))) return rc;
+  if ((rc = h2d(ctx, ctx->buf[BUF_Y], colors, 3 * n * sizeof(double), dev))) return rc;
+  if (!dev && (rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false))) return rc;
+  if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
+  if ((rc = stage_graph(ctx, dev ? coords : ctx->coords64, n, bits, true, w64))) return rc;
+  if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
+
+  fgbd_noise nz;
+  std::memset(&nz, 0, sizeof(nz));
+  if (cached_q >= 0) {
+    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
+    int fin = BUF_Y;
+    if ((rc = launch_fixed_steps(ctx, n, cached_q, w64, &fin))) return rc;
+    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
+    if ((rc = launch_finalize(ctx, n, fin, ctx->out))) return rc;
+  } else {
+    const int D = cfg->patch_size;
+    if ((rc = launch_noise(ctx, n, D))) return rc;
+    if ((rc = pull_ctl(ctx))) return rc;
+    if ((rc = check_graph_ctl(ctx, bits))) return rc;
+    const int maxdeg = ctx->ctl_host->max_deg;
+    if (D > 1 + maxdeg)
+      return set_error(ctx, FGBD_E_NOISE, "patch_size " + std::to_string(D) +
+                                              " exceeds 1 + max degree (" +
+                                              std::to_string(1 + maxdeg) + ") of this graph");
+    if ((rc = finish_noise(ctx, D, cfg->tau_divisor, &nz))) return rc;
+    const double sig = nz.sigma_est;
+    const int active = cfg->fslr_enabled && !(sig < cfg->fslr_sigma_floor);
+    if ((rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode, nullptr)))
+      return rc;
+    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
+    if ((rc = launch_select_steps(ctx, n, cfg->q_max, cfg->criterion_mode, cfg->early_exit, sig,
+                                  w64)))
+      return rc;
+    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
+    if ((rc = launch_finalize(ctx, n, -1, ctx->out))) return rc;
+  }
+  if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
+  if ((rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), dev))) return rc;
+  if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
+  if ((rc = pull_ctl(ctx))) return rc;
+  if ((rc = check_graph_ctl(ctx, bits))) return rc;
+  const Ctl& h = *ctx->ctl_host;
+  rep->n_edges = (int64_t)h.n_edges;
+  rep->nnz = 2 * (int64_t)h.n_edges;
+  rep->max_degree = h.max_deg;
+  rep->sigma_g = h.sigma_g;
+  if (cached_q >= 0) {
+    rep->selected_q = cached_q;
+    rep->sigma_est = std::isnan(cached_sigma) ? 0.0 : cached_sigma;
+    rep->masked_fraction = 0.0;
+    rep->cached = 1;
+    rep->steps = cached_q;
+  } else {
+    rep->selected_q = h.best_q;
+    rep->sigma_est = nz.sigma_est;
+    rep->masked_fraction = 1.0 - (double)h.included / (double)n;
+    rep->criterion_value = h.best_crit;
+    const double eps = std::isnan(cfg->epsilon) ? 1e-3 * nz.sigma_est * nz.sigma_est : cfg->epsilon;
+    rep->converged = h.best_crit <= eps ? 1 : 0;
+    rep->steps = h.steps;
+    rep->all_excluded_fallback = h.all_excluded;
+    rep->included_count = h.included;
+    fill_noise_report(rep, nz);
+    rep->n_trace = std::min(h.steps + 1, FGBD_TRACE_MAX);
+    for (int k = 0; k < rep->n_trace; ++k) rep->trace[k] = h.trace[k];
+  }
+  if (timing) {
+    rep->t_graph_construction = ev_sec(ev[1], ev[2]);
+    rep->t_noise_estimation = cached_q >= 0 ? 0.0 : ev_sec(ev[2], ev[3]);
+    rep->t_low_pass_filter = ev_sec(ev[3], ev[4]);
+    rep->t_total = ev_sec(ev[0], ev[5]);
+    rep->t_lf_steps = ev_sec(ev[3], ev[6]);
+  }
+  rep->gpu_launches = ctx->launches;
+  return FGBD_OK;
+}
+
+int32_t fgbd_radix_argsort(fgbd_ctx* ctx, const uint64_t* keys, int64_t n, int32_t key_bits,
+                           int64_t* perm_out, uint32_t flags) {
+  if (!ctx) return set_error(ctx, FGBD_E_ARG, "null context");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  if (key_bits < 1 || key_bits > 64)
+    return set_error(ctx, FGBD_E_ARG, "key_bits must be in [1, 64], got " + std::to_string(key_bits));
+  if (n >= (int64_t(1) << 31)) return set_error(ctx, FGBD_E_ARG, "n too large");
+  const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
+  if (n < 2) {
+    const int64_t zero = 0;
+    if (n == 1) FGBD_CUDA(ctx, cudaMemcpy(perm_out, &zero, 8, cudaMemcpyDefault));
+    return FGBD_OK;
+  }
+  int rc = ensure_capacity(ctx, n, 1);
+  if (rc) return rc;
+  if ((rc = h2d(ctx, ctx->coords64, keys, n * sizeof(uint64_t), dev))) return rc;
+  uint32_t* d_perm = nullptr;
+  if ((rc = launch_argsort64(ctx, (const uint64_t*)ctx->coords64, n, key_bits, &d_perm))) return rc;
+  std::vector<uint32_t> h(n);
+  FGBD_CUDA(ctx, cudaMemcpyAsync(h.data(), d_perm, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (dev) {
+    std::vector<int64_t> w(h.begin(), h.end());
+    FGBD_CUDA(ctx, cudaMemcpy(perm_out, w.data(), n * 8, cudaMemcpyHostToDevice));
+  } else {
+    for (int64_t i = 0; i < n; ++i) perm_out[i] = h[i];
+  }
+  ctx->g_n = -1;  // sort scratch reused: the held graph is gone
+  return FGBD_OK;
+}
+
+int32_t fgbd_scan_line(fgbd_ctx* ctx, const int64_t* coords, int64_t n, int32_t bits,
+                       int32_t line, uint64_t* codes_out, int64_t* perm_out, uint32_t flags) {
+  if (!ctx) return set_error(ctx, FGBD_E_ARG, "null context");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  int rc = check_graph_input(ctx, n, bits);
+  if (rc) return rc;
+  if (line < 1 || line > 3)
+    return set_error(ctx, FGBD_E_GRAPH, "line must be 1, 2 or 3, got " + std::to_string(line));
+  const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
+  if (n < 1) return FGBD_OK;
+  if ((rc = ensure_capacity(ctx, n, 3 * bits > 32))) return rc;
+  if ((rc = reset_ctl(ctx))) return rc;
+  if (dev) ctx->cur_coords = coords;
+  else {
+    if ((rc = h2d(ctx, ctx->coords64, coords, 3 * n * 8, false))) return rc;
+    ctx->cur_coords = ctx->coords64;
+  }
+  uint32_t* d_perm = nullptr;
+  uint64_t* d_codes = (uint64_t*)ctx->out;  // (3n doubles) >= n codes
+  if ((rc = launch_scan_line(ctx, n, bits, line - 1, d_codes, &d_perm))) return rc;
+  if (codes_out) {
+    if ((rc = d2h(ctx, codes_out, d_codes, n * 8, dev))) return rc;
+  }
+  std::vector<uint32_t> h(n);
+  FGBD_CUDA(ctx, cudaMemcpyAsync(h.data(), d_perm, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if ((rc = pull_ctl(ctx))) return rc;
+  if (ctx->ctl_host->err_flags & 1)
+    return set_error(ctx, FGBD_E_CLOUD, "coordinates out of range for bit_depth=" + std::to_string(bits));
+  if (perm_out) {
+    if (dev) {
+      std::vector<int64_t> w(h.begin(), h.end());
+      FGBD_CUDA(ctx, cudaMemcpy(perm_out, w.data(), n * 8, cudaMemcpyHostToDevice));
+    } else {
+      for (int64_t i = 0; i < n; ++i) perm_out[i] = h[i];
+    }
+  }
+  ctx->g_n = -1;
+  return FGBD_OK;
+}
+
+int32_t fgbd_build_graph(fgbd_ctx* ctx, const int64_t* coords, int64_t n, int32_t bits,
+                         fgbd_graph_info* info, uint32_t flags) {
+  if (!ctx || !info) return set_error(ctx, FGBD_E_ARG, "null argument");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  std::memset(info, 0, sizeof(*info));
+  info->n = n;
+  int rc = check_graph_input(ctx, n, bits);
+  if (rc) return rc;
+  if (n < 2) {
+    ctx->g_n = n;
+    ctx->g_bits = bits;
+    return FGBD_OK;
+  }
+  const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
+  if ((rc = stage_graph(ctx, coords, n, bits, dev, (flags & FGBD_FLAG_WEIGHTS_F64) ? 1 : 0)))
+    return rc;
+  if ((rc = pull_ctl(ctx))) return rc;
+  const Ctl& h = *ctx->ctl_host;
+  if (h.err_flags & 1) {
+    ctx->g_n = -1;
+    return set_error(ctx, FGBD_E_CLOUD, "coordinates out of range for bit_depth=" + std::to_string(bits));
+  }
+  info->n_edges = (int64_t)h.n_edges;
+  info->nnz = 2 * (int64_t)h.n_edges;
+  info->max_degree = h.max_deg;
+  info->sigma_g = h.sigma_g;
+  return FGBD_OK;
+}
+
+int32_t fgbd_graph_export(fgbd_ctx* ctx, int64_t* indptr, int64_t* indices, int64_t* csr_edge,
+                          int64_t* edge_u, int64_t* edge_v, double* edge_sqdist,
+                          double* edge_weights, double* wdeg) {
+  if (!ctx) return set_error(ctx, FGBD_E_ARG, "null context");
+  cudaSetDevice(ctx->device);
+  if (ctx->g_n < 0) return set_error(ctx, FGBD_E_GRAPH, "no graph held by this context");
+  const int64_t n = ctx->g_n;
+  if (n < 2) {
+    if (indptr)
+      for (int64_t i = 0; i <= n; ++i) indptr[i] = 0;
+    if (wdeg)
+      for (int64_t i = 0; i < n; ++i) wdeg[i] = 0.0;
+    return FGBD_OK;
+  }
+  if ((int)pull_ctl(ctx)) return FGBD_E_CUDA;
+  const int64_t E = (int64_t)ctx->ctl_host->n_edges, nnz = 2 * E;
+  // device staging, one allocation
+  const size_t bytes = (size_t)(n + 1 + 2 * nnz + 2 * E) * 8 + (size_t)(2 * E + n) * 8;
+  char* d = nullptr;
+  FGBD_CUDA(ctx, cudaMalloc(&d, bytes));
+  int64_t* d_indptr = (int64_t*)d;
+  int64_t* d_indices = d_indptr + n + 1;
+  int64_t* d_csr = d_indices + nnz;
+  int64_t* d_u = d_csr + nnz;
+  int64_t* d_v = d_u + E;
+  double* d_sq = (double*)(d_v + E);
+  double* d_w = d_sq + E;
+  double* d_wd = d_w + E;
+  int64_t nnz2 = 0, e2 = 0;
+  int rc = launch_export(ctx, n, d_indptr, d_indices, d_csr, d_u, d_v, d_sq, d_w, d_wd, &nnz2, &e2);
+  if (rc == FGBD_OK && (nnz2 != nnz || e2 != E))
+    rc = set_error(ctx, FGBD_E_GRAPH, "internal: edge count mismatch in export");
+  auto cp = [&](void* dst, const void* src, size_t b) {
+    if (dst && rc == FGBD_OK && b) {
+      cudaError_t e = cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) rc = cuda_error(ctx, e, "export copy");
+    }
+  };
+  cp(indptr, d_indptr, (n + 1) * 8);
+  cp(indices, d_indices, nnz * 8);
+  cp(csr_edge, d_csr, nnz * 8);
+  cp(edge_u, d_u, E * 8);
+  cp(edge_v, d_v, E * 8);
+  cp(edge_sqdist, d_sq, E * 8);
+  cp(edge_weights, d_w, E * 8);
+  cp(wdeg, d_wd, n * 8);
+  cudaFree(d);
+  return rc;
+}
+
+int32_t fgbd_estimate_noise(fgbd_ctx* ctx, const double* colors, int32_t patch_size,
+                            int32_t tau_divisor, fgbd_noise* out, double* fslr_stat_out,
+                            uint32_t flags) {
+  if (!ctx || !out) return set_error(ctx, FGBD_E_ARG, "null argument");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  std::memset(out, 0, sizeof(*out));
+  if (ctx->g_n < 0) return set_error(ctx, FGBD_E_GRAPH, "no graph held by this context");
+  const int64_t n = ctx->g_n;
+  const int D = patch_size;
+  if (D < 2) return set_error(ctx, FGBD_E_NOISE, "patch_size must be >= 2, got " + std::to_string(D));
+  int maxdeg = 0;
+  if (n >= 2) {
+    if (pull_ctl(ctx)) return FGBD_E_CUDA;
+    maxdeg = ctx->ctl_host->max_deg;
+  }
+  if (D > 1 + maxdeg)
+    return set_error(ctx, FGBD_E_NOISE, "patch_size " + std::to_string(D) +
+                                            " exceeds 1 + max degree (" + std::to_string(1 + maxdeg) +
+                                            ") of this graph");
+  const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
+  int rc = h2d(ctx, ctx->buf[BUF_Y], colors, 3 * n * sizeof(double), dev);
+  if (rc) return rc;
+  if ((rc = launch_noise(ctx, n, D))) return rc;
+  if ((rc = pull_ctl(ctx))) return rc;
+  if ((rc = finish_noise(ctx, D, tau_divisor, out))) return rc;
+  if (fslr_stat_out) {
+    if ((rc = d2h(ctx, fslr_stat_out, ctx->fslr, n * sizeof(double), dev))) return rc;
+    FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  ctx->g_have_noise = 1;
+  ctx->g_patch = D;
+  return FGBD_OK;
+}
+
+int32_t fgbd_fslr_mask(fgbd_ctx* ctx, double sigma_est, double sigma_floor, uint8_t* include_out,
+                       int32_t* all_excluded) {
+  if (!ctx || !include_out) return set_error(ctx, FGBD_E_ARG, "null argument");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  if (all_excluded) *all_excluded = 0;
+  if (!ctx->g_have_noise)
+    return set_error(ctx, FGBD_E_NOISE, "run fgbd_estimate_noise before fgbd_fslr_mask");
+  const int64_t n = ctx->g_n;
+  const int active = !(sigma_est < sigma_floor);
+  int rc = launch_mask(ctx, n, sigma_est, active, 0, FGBD_CRIT_POOLED, nullptr);
+  if (rc) return rc;
+  std::vector<uint32_t> bits((n + 31) / 32);
+  FGBD_CUDA(ctx, cudaMemcpyAsync(bits.data(), ctx->mask, bits.size() * 4, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  if ((rc = pull_ctl(ctx))) return rc;
+  for (int64_t i = 0; i < n; ++i) include_out[i] = (bits[i >> 5] >> (i & 31)) & 1u;
+  if (ctx->ctl_host->all_excluded) {
+    if (all_excluded) *all_excluded = 1;
+    return set_error(ctx, FGBD_E_FILTER,
+                     "the variance threshold excluded every point; fall back to unmasked "
+                     "selection (disable the mask or raise sigma_floor)");
+  }
+  return FGBD_OK;
+}
+
+int32_t fgbd_filter_steps_csr(fgbd_ctx* ctx, const int64_t* indptr, const int64_t* indices,
+                              const double* slot_weights, int64_t n, int64_t nnz,
+                              const double* colors_in, int32_t q, double* colors_out,
+                              uint32_t flags) {
+  if (!ctx) return set_error(ctx, FGBD_E_ARG, "null context");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  if (q < 0) return set_error(ctx, FGBD_E_FILTER, "q must be >= 0, got " + std::to_string(q));
+  if (n < 1) return FGBD_OK;
+  const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
+  const size_t bytes = (size_t)(n + 1 + nnz) * 8 + (size_t)nnz * 8 + (size_t)9 * n * 8;
+  char* d = nullptr;
+  FGBD_CUDA(ctx, cudaMalloc(&d, bytes));
+  int64_t* d_ip = (int64_t*)d;
+  int64_t* d_ix = d_ip + n + 1;
+  double* d_w = (double*)(d_ix + nnz);
+  double* d_in = d_w + nnz;
+  double* d_tmp = d_in + 3 * n;
+  double* d_out = d_tmp + 3 * n;
+  int rc = FGBD_OK;
+  auto up = [&](void* dst, const void* src, size_t b) {
+    if (rc == FGBD_OK && b) {
+      cudaError_t e = cudaMemcpy(dst, src, b, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) rc = cuda_error(ctx, e, "csr upload");
+    }
+  };
+  up(d_ip, indptr, (n + 1) * 8);
+  up(d_ix, indices, nnz * 8);
+  up(d_w, slot_weights, nnz * 8);
+  up(d_in, colors_in, 3 * n * 8);
+  if (rc == FGBD_OK) rc = launch_csr_steps(ctx, d_ip, d_ix, d_w, n, d_in, d_tmp, d_out, q);
+  if (rc == FGBD_OK) {
+    cudaError_t e = cudaMemcpyAsync(colors_out, d_out, 3 * n * 8,
+                                    dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                    ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = cuda_error(ctx, e, "csr download");
+  }
+  cudaFree(d);
+  return rc;
+}
+
+int32_t fgbd_apply_filter(fgbd_ctx* ctx, const double* colors_in, int32_t q, double* colors_out,
+                          uint32_t flags) {
+  if (!ctx) return set_error(ctx, FGBD_E_ARG, "null context");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  if (q < 0) return set_error(ctx, FGBD_E_FILTER, "q must be >= 0, got " + std::to_string(q));
+  if (ctx->g_n < 0) return set_error(ctx, FGBD_E_GRAPH, "no graph held by this context");
+  const int64_t n = ctx->g_n;
+  const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
+  if (n < 2) {
+    if (n) FGBD_CUDA(ctx, cudaMemcpy(colors_out, colors_in, 3 * n * 8, cudaMemcpyDefault));
+    return FGBD_OK;
+  }
+  int rc = h2d(ctx, ctx->buf[BUF_Y], colors_in, 3 * n * 8, dev);
+  if (rc) return rc;
+  int fin = BUF_Y;
+  if ((rc = launch_fixed_steps(ctx, n, q, ctx->g_weights64, &fin))) return rc;
+  if ((rc = d2h(ctx, colors_out, ctx->buf[fin], 3 * n * 8, dev))) return rc;
+  FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FGBD_OK;
+}
+
+int32_t fgbd_select_q(fgbd_ctx* ctx, const double* colors, const uint8_t* include,
+                      double sigma_est, const fgbd_config* cfg, int32_t* q_out, double* x_out,
+                      fgbd_report* rep, uint32_t flags) {
+  if (!ctx || !cfg) return set_error(ctx, FGBD_E_ARG, "null argument");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  int rc = check_cfg(ctx, cfg);
+  if (rc) return rc;
+  if (sigma_est < 0) {
+    char b[96];
+    std::snprintf(b, sizeof(b), "sigma_est must be >= 0, got %.17g", sigma_est);
+    return set_error(ctx, FGBD_E_FILTER, b);
+  }
+  if (ctx->g_n < 0) return set_error(ctx, FGBD_E_GRAPH, "no graph held by this context");
+  const int64_t n = ctx->g_n;
+  const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
+  if ((rc = h2d(ctx, ctx->buf[BUF_Y], colors, 3 * n * 8, dev))) return rc;
+  uint8_t* d_inc = nullptr;
+  std::vector<uint8_t> ones;
+  if (include) {
+    FGBD_CUDA(ctx, cudaMalloc(&d_inc, n));
+    cudaError_t e = cudaMemcpy(d_inc, include, n, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(d_inc);
+      return cuda_error(ctx, e, "include upload");
+    }
+  } else {
+    ones.assign(n, 1);
+    FGBD_CUDA(ctx, cudaMalloc(&d_inc, n));
+    FGBD_CUDA(ctx, cudaMemcpy(d_inc, ones.data(), n, cudaMemcpyHostToDevice));
+  }
+  rc = launch_mask(ctx, n, sigma_est, 0, cfg->q_max, cfg->criterion_mode, d_inc);
+  if (rc == FGBD_OK)
+    rc = launch_select_steps(ctx, n, cfg->q_max, cfg->criterion_mode, cfg->early_exit, sigma_est,
+                             ctx->g_weights64);
+  if (rc == FGBD_OK) rc = pull_ctl(ctx);
+  cudaFree(d_inc);
+  if (rc) return rc;
+  const Ctl& h = *ctx->ctl_host;
+  if (h.included < 1)
+    return set_error(ctx, FGBD_E_FILTER, "criterion needs at least one included point");
+  if (q_out) *q_out = h.best_q;
+  if (x_out) {
+    if ((rc = d2h(ctx, x_out, ctx->buf[h.best_buf], 3 * n * 8, dev))) return rc;
+    FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->selected_q = h.best_q;
+    rep->sigma_est = sigma_est;
+    rep->criterion_value = h.best_crit;
+    rep->steps = h.steps;
+    rep->included_count = h.included;
+    rep->masked_fraction = 1.0 - (double)h.included / (double)n;
+    rep->n_trace = std::min(h.steps + 1, FGBD_TRACE_MAX);
+    for (int k = 0; k < rep->n_trace; ++k) rep->trace[k] = h.trace[k];
+  }
+  return FGBD_OK;
+}
+
+int32_t fgbd_selection_criterion(fgbd_ctx* ctx, const double* y, const double* x,
+                                 const uint8_t* include, int64_t n, double sigma_est, int32_t mode,
+                                 double* crit_out, uint32_t flags) {
+  if (!ctx || !crit_out) return set_error(ctx, FGBD_E_ARG, "null argument");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  if (mode != FGBD_CRIT_POOLED && mode != FGBD_CRIT_PER_CHANNEL)
+    return set_error(ctx, FGBD_E_FILTER, "unknown criterion mode");
+  if (n < 1) return set_error(ctx, FGBD_E_FILTER, "criterion needs at least one included point");
+  const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
+  char* d = nullptr;
+  FGBD_CUDA(ctx, cudaMalloc(&d, 6 * n * 8 + n));
+  double* d_y = (double*)d;
+  double* d_x = d_y + 3 * n;
+  uint8_t* d_inc = include ? (uint8_t*)(d_x + 3 * n) : nullptr;
+  const cudaMemcpyKind k = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  cudaError_t e = cudaMemcpy(d_y, y, 3 * n * 8, k);
+  if (e == cudaSuccess) e = cudaMemcpy(d_x, x, 3 * n * 8, k);
+  if (e == cudaSuccess && include) e = cudaMemcpy(d_inc, include, n, k);
+  int rc = e == cudaSuccess ? launch_criterion(ctx, d_y, d_x, d_inc, n, sigma_est, mode, crit_out)
+                            : cuda_error(ctx, e, "criterion upload");
+  cudaFree(d);
+  return rc;
+}
+
+int32_t fgbd_symmetric_eigenvalues(const double* s, int32_t d, double* out_desc, char* err,
+                                   int32_t err_len) {
+  std::string msg;
+  if (d < 1) msg = "matrix must be square";
+  int rc = d < 1 ? FGBD_E_NOISE : jacobi_eigenvalues(s, d, out_desc, &msg);
+  if (rc && err && err_len > 0) std::snprintf(err, err_len, "%s", msg.c_str());
+  return rc;
+}
+
+int32_t fgbd_select_tail(const double* lam, int32_t d, int32_t tau_divisor, int32_t* m,
+                         double* tau, int32_t* fallback, char* err, int32_t err_len) {
+  std::string msg;
+  int mm = 0, fb = 0;
+  double t = 0;
+  int rc = select_tail_host(lam, d, tau_divisor, &mm, &t, &fb, &msg);
+  if (rc) {
+    if (err && err_len > 0) std::snprintf(err, err_len, "%s", msg.c_str());
+    return rc;
+  }
+  *m = mm;
+  *tau = t;
+  *fallback = fb;
+  return FGBD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,194 @@
+// Internal declarations shared by the FGBD B200 translation units.
+//
+// Device data layout for one frame of N points:
+//   pc        packed coordinates = the line-1 scan code z<<2b | y<<b | x,
+//             uint32 when 3b <= 32 else uint64 (4 or 8 B/pt)
+//   sort      per line: keys/vals ping-pong + onesweep look-back status
+//   perm      per line: stable rank order (uint32, the sort's last pass)
+//   cand      per line: (prev, next) rank neighbour, int2 (24 B/pt total)
+//   ell       6 slots per point, slot-major [s][N], int2 = (neighbour,
+//             payload) where payload is the exact squared distance (uint32)
+//             until the weight pass replaces it by the fp32 Gaussian weight;
+//             padding slots hold (self, 0)
+//   meta      per point: degree (3 bits) | patch order (6 x 3 bits)
+//   buf[3]    fp64 (N,3) signals: Y = noisy input, A, B (select_q rotation)
+//   fslr      per point FSLR statistic (fp64, -1 = not eligible)
+//   mask      1 bit per point (FSLR include)
+//   ctl       device control block (reductions, select_q state)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "fgbd_b200.h"
+
+namespace fgbd {
+
+constexpr int kBlock = 256;
+constexpr int kRedGrid = 148 * 4;      // fixed partition => deterministic sums
+constexpr int kNeGrid = 148 * 6;       // NE blocks (96 threads: one warp per channel)
+constexpr int kSortThreads = 256;
+constexpr int kSortIPT = 16;
+constexpr int kSortTile = kSortThreads * kSortIPT;  // keys per onesweep tile
+constexpr int kRadix = 256;
+constexpr int kMaxPasses = 8;
+constexpr int kSlots = 6;              // max SLG degree: 2 neighbours x 3 lines
+constexpr int kMom = 35;               // 7 first + 28 second moments per channel
+
+enum BufId { BUF_Y = 0, BUF_A = 1, BUF_B = 2 };
+
+// Device control block.  Written by "last block done" reducers, read by the
+// next kernel in stream order and mirrored to pinned host memory.
+struct Ctl {
+  // graph construction
+  unsigned long long n_edges;
+  double sigma_g;
+  int max_deg;
+  int err_flags;  // bit0: coordinate out of range
+  // noise estimation
+  long long eligible;
+  double mom[3][kMom];
+  // FSLR mask
+  long long included;
+  int mask_all;
+  int all_excluded;
+  double sy[3];
+  // select_q state machine (filtering.py:225-256)
+  int q;
+  int best_q;
+  int stop;
+  int streak;
+  int steps;
+  int in_buf;
+  int out_buf;
+  int best_buf;
+  double best_crit;
+  double prev_crit;
+  double trace[FGBD_TRACE_MAX];
+  unsigned int ticket[8];
+};
+
+struct SortScratch {
+  void* keys[2][3] = {};        // ping-pong key buffers per line
+  uint32_t* vals[2][3] = {};    // ping-pong value buffers per line
+  uint32_t* hist = nullptr;     // [3][kMaxPasses][256] counts -> bases
+  unsigned long long* status = nullptr;  // [3][tiles][256] look-back words
+  unsigned int* tile_ctr = nullptr;      // [kMaxPasses][3]
+  int64_t tiles_cap = 0;
+  unsigned int epoch = 0;
+};
+
+}  // namespace fgbd
+
+struct fgbd_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  int64_t cap = 0;        // points the scratch is sized for
+  int key64_cap = 0;      // scratch sized for 64-bit keys
+  size_t dev_bytes = 0;
+
+  int64_t* coords64 = nullptr;  // (N,3) int64 staging (H2D target)
+  const int64_t* cur_coords = nullptr;  // coordinates of the frame being built (device)
+  double** d_bufs = nullptr;    // device copy of buf[] (for ctl-selected buffers)
+  void* pc = nullptr;           // packed coords (uint32 or uint64)
+  fgbd::SortScratch sort;
+  uint32_t* perm[3] = {};       // aliases into sort.vals after the last pass
+  int2* cand = nullptr;         // [3][N]
+  int2* ell = nullptr;          // [6][N]
+  double* w64 = nullptr;        // [6][N] fp64 weights (parity mode, lazy)
+  uint32_t* meta = nullptr;     // [N]
+  double* buf[3] = {};          // Y, A, B signals (N,3) fp64
+  double* out = nullptr;        // (N,3) fp64 result staging
+  double* fslr = nullptr;       // [N]
+  uint32_t* mask = nullptr;     // [ceil(N/32)]
+  double* partials = nullptr;   // reduction partials
+  fgbd::Ctl* ctl = nullptr;     // device
+  fgbd::Ctl* ctl_host = nullptr;  // pinned mirror
+  // scratch for CSR export / injection (lazy)
+  int64_t* scan_tmp = nullptr;
+  int64_t scan_cap = 0;
+  void* csr_scratch = nullptr;
+  size_t csr_scratch_bytes = 0;
+
+  cudaEvent_t ev[8] = {};
+
+  // state of the graph held by the context
+  int64_t g_n = -1;
+  int g_bits = 0;
+  int g_weights64 = 0;
+  int g_have_weights = 0;
+  int g_have_noise = 0;
+  int g_patch = 0;
+
+  int launches = 0;
+  std::string err;
+};
+
+namespace fgbd {
+
+// ---- error plumbing ------------------------------------------------------
+int set_error(fgbd_ctx* ctx, int code, const std::string& msg);
+int cuda_error(fgbd_ctx* ctx, cudaError_t e, const char* where);
+#define FGBD_CUDA(ctx, call)                                   \
+  do {                                                         \
+    cudaError_t e__ = (call);                                  \
+    if (e__ != cudaSuccess) return fgbd::cuda_error(ctx, e__, #call); \
+  } while (0)
+#define FGBD_LAUNCH(ctx)                                       \
+  do {                                                         \
+    (ctx)->launches++;                                         \
+    cudaError_t e__ = cudaGetLastError();                      \
+    if (e__ != cudaSuccess) return fgbd::cuda_error(ctx, e__, "kernel launch"); \
+  } while (0)
+
+int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64);
+int ensure_w64(fgbd_ctx* ctx, int64_t n);
+
+// ---- graph construction (graph.cu) --------------------------------------
+// Builds pc, sorts the 3 scan lines, writes cand/ell/meta, reduces sigma_g.
+// coords64 already on device.  No host sync.
+int launch_graph(fgbd_ctx* ctx, int64_t n, int bits);
+// Converts the ell payload (squared distances) into Gaussian weights.
+int launch_weights(fgbd_ctx* ctx, int64_t n, int bits, int w64);
+// Stand-alone stable argsort of 64-bit keys (radix_argsort).
+int launch_argsort64(fgbd_ctx* ctx, const uint64_t* d_keys, int64_t n, int key_bits,
+                     uint32_t** d_perm_out);
+// Codes + perm for one line of the frame (codes written as uint64).
+int launch_scan_line(fgbd_ctx* ctx, int64_t n, int bits, int line, uint64_t* d_codes,
+                     uint32_t** d_perm_out);
+// CSR export helpers (device): writes reference-convention arrays.
+int launch_export(fgbd_ctx* ctx, int64_t n, int64_t* d_indptr, int64_t* d_indices,
+                  int64_t* d_csr_edge, int64_t* d_edge_u, int64_t* d_edge_v,
+                  double* d_sqdist, double* d_weights, double* d_wdeg,
+                  int64_t* nnz_out, int64_t* e_out);
+
+// exclusive scan of int64 (3 launches); tmp >= ceil(n/2048), *d_total gets the sum
+int scan_exclusive(fgbd_ctx* ctx, const int64_t* in, int64_t n, int64_t* out, int64_t* tmp,
+                   int64_t* d_total);
+
+// ---- noise estimation (noise.cu) ----------------------------------------
+int launch_noise(fgbd_ctx* ctx, int64_t n, int patch);
+// host side: covariance -> Jacobi -> tail -> sigma (noise.py:122-243)
+int finish_noise(fgbd_ctx* ctx, int patch, int divisor, fgbd_noise* out);
+int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err);
+int select_tail_host(const double* lam, int d, int divisor, int* m, double* tau,
+                     int* fallback, std::string* err);
+
+// ---- filter (filter.cu) --------------------------------------------------
+int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active,
+                int q_max, int mode, const uint8_t* d_include_bytes);
+int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int mode, int early_exit,
+                        double sigma_est, int w64);
+int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf);
+int launch_finalize(fgbd_ctx* ctx, int64_t n, int src_buf_or_neg, double* d_out);
+int launch_csr_steps(fgbd_ctx* ctx, const int64_t* d_indptr, const int64_t* d_indices,
+                     const double* d_w, int64_t n, const double* d_in, double* d_tmp,
+                     double* d_out, int q);
+int launch_criterion(fgbd_ctx* ctx, const double* d_y, const double* d_x,
+                     const uint8_t* d_inc, int64_t n, double sigma_est, int mode,
+                     double* crit_out);
+
+}  // namespace fgbd

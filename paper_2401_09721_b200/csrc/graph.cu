@@ -1,0 +1,794 @@
+// Scan-line graph construction on sm_100a (reference graph.py:122-251).
+//
+//   k_prep       coords int64 -> packed line-1 code (pc) + digit histograms
+//                of all three scan lines for every radix pass (one read)
+//   k_scan_hist  histograms -> exclusive digit bases
+//   k_onesweep   one stable LSD pass for all three lines: warp multisplit
+//                (match.any) -> decoupled look-back across tiles -> smem
+//                reorder -> coalesced scatter (8-bit digits, ceil(3b/8)
+//                passes, exactly the reference's pass count, graph.py:168)
+//   k_neighbors  rank neighbours: cand[l][perm_l[k]] = (perm_l[k-1], perm_l[k+1])
+//   k_rows       per point: sort + dedup <= 6 candidates (the reference's
+//                np.unique + lexsort, graph.py:188-208), exact squared
+//                lengths, patch order by (sqdist, index) (noise.py:112),
+//                sigma_g partial sums (graph.py:227-233)
+//   k_weights    Eq. (4): w = exp(-sqdist / sigma_g^2) (graph.py:236-245)
+//   k_export_*   reference CSR / edge-list conventions for the stage API
+#include <algorithm>
+#include <cstdio>
+
+#include "device_util.cuh"
+#include "fgbd_internal.cuh"
+
+namespace fgbd {
+
+// ---------------------------------------------------------------------------
+// codes
+// ---------------------------------------------------------------------------
+
+// line 0: pc itself (z, y, x); line 1: (x, z, y); line 2: (y, x, z) -- graph.py:25
+template <typename K>
+__device__ __forceinline__ K line_key(K pc, int line, int b) {
+  if (line == 0) return pc;
+  const K m = (K(1) << b) - 1;
+  const K x = pc & m, y = (pc >> b) & m, z = pc >> (2 * b);
+  if (line == 1) return (x << (2 * b)) | (z << b) | y;
+  return (y << (2 * b)) | (x << b) | z;
+}
+
+template <typename K>
+__device__ __forceinline__ void unpack(K pc, int b, long long* x, long long* y, long long* z) {
+  const K m = (K(1) << b) - 1;
+  *x = (long long)(pc & m);
+  *y = (long long)((pc >> b) & m);
+  *z = (long long)(pc >> (2 * b));
+}
+
+// Histogram of every digit of every line, warp-aggregated smem atomics.
+template <typename K, bool FROM_COORDS>
+__global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coords,
+                                                 const K* __restrict__ keys_in, int64_t n,
+                                                 int b, int nlines, int passes,
+                                                 K* __restrict__ pc, uint32_t* __restrict__ hist,
+                                                 Ctl* __restrict__ ctl) {
+  extern __shared__ uint32_t s_hist[];  // [nlines][passes][256]
+  const int nh = nlines * passes * kRadix;
+  for (int t = threadIdx.x; t < nh; t += blockDim.x) s_hist[t] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long lim = (1ll << b);
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool valid = i < n;
+    K code = 0;
+    if (valid) {
+      if (FROM_COORDS) {
+        const long long x = coords[3 * i], y = coords[3 * i + 1], z = coords[3 * i + 2];
+        bad |= (x < 0) | (y < 0) | (z < 0) | (x >= lim) | (y >= lim) | (z >= lim);
+        code = (K(z) << (2 * b)) | (K(y) << b) | K(x);
+        pc[i] = code;
+      } else {
+        code = keys_in[i];
+      }
+    }
+    for (int l = 0; l < nlines; ++l) {
+      const K key = FROM_COORDS ? line_key(code, l, b) : code;
+      for (int p = 0; p < passes; ++p) {
+        const unsigned d = valid ? (unsigned)((key >> (8 * p)) & 0xff) : 0x100u;
+        const unsigned peers = __match_any_sync(kFull, d);
+        const int leader = 31 - __clz(peers);
+        if (valid && lane == leader)
+          atomicAdd(&s_hist[(l * passes + p) * kRadix + d], (uint32_t)__popc(peers));
+      }
+    }
+  }
+  if (bad) atomicOr(&ctl->err_flags, 1);
+  __syncthreads();
+  for (int t = threadIdx.x; t < nh; t += blockDim.x)
+    if (s_hist[t]) atomicAdd(&hist[t], s_hist[t]);
+}
+
+// Exclusive scan of each 256-bin histogram, in place.  One block of 256.
+__global__ void k_scan_hist(uint32_t* hist, int nhist) {
+  __shared__ uint32_t s_w[8];
+  const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+  for (int h = 0; h < nhist; ++h) {
+    const uint32_t c = hist[h * kRadix + d];
+    uint32_t v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, v, o);
+      if (lane >= o) v += t;
+    }
+    if (lane == 31) s_w[warp] = v;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int w = 0; w < warp; ++w) off += s_w[w];
+    hist[h * kRadix + d] = off + v - c;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// onesweep pass
+// ---------------------------------------------------------------------------
+
+struct SortPass {
+  const void* src_keys[3];      // null on pass 0 in SLG mode (keys from pc)
+  const void* pc;
+  const uint32_t* src_vals[3];  // null on pass 0 (identity)
+  void* dst_keys[3];
+  uint32_t* dst_vals[3];
+  const uint32_t* bases;        // [line][passes][256]
+  unsigned long long* status;   // [line][tiles][256]
+  unsigned int* tile_ctr;       // [line]
+  int64_t n;
+  int b, pass, passes, tiles;
+  unsigned int epoch;
+};
+
+constexpr unsigned long long kFlagAgg = 1ull << 32;
+constexpr unsigned long long kFlagPre = 2ull << 32;
+
+template <typename K, bool FIRST, bool LAST, bool SLG>
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(SortPass p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  K* s_keys = reinterpret_cast<K*>(smem);
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kSortTile);
+  uint32_t* s_whist = s_vals + kSortTile;  // [8 warps][256]
+  __shared__ uint32_t s_start[kRadix];    // tile-local exclusive digit start
+  __shared__ uint32_t s_gofs[kRadix];     // global position - local index
+  __shared__ uint32_t s_wsum[8];
+  __shared__ int s_tile;
+
+  const int line = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = (int)atomicAdd(&p.tile_ctr[line], 1u);
+  for (int t = tid; t < 8 * kRadix; t += kSortThreads) s_whist[t] = 0;
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = (int64_t)tile * kSortTile;
+  const int shift = 8 * p.pass;
+
+  K key[kSortIPT];
+  uint32_t val[kSortIPT];
+  uint32_t loc[kSortIPT];
+  const K* kin = reinterpret_cast<const K*>(p.src_keys[line]);
+  const K* pcp = reinterpret_cast<const K*>(p.pc);
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j) {
+    const int64_t idx = base + (int64_t)warp * 32 * kSortIPT + j * 32 + lane;
+    if (idx < p.n) {
+      if (FIRST) {
+        key[j] = SLG ? line_key(pcp[idx], line, p.b) : kin[idx];
+        val[j] = (uint32_t)idx;
+      } else {
+        key[j] = kin[idx];
+        val[j] = p.src_vals[line][idx];
+      }
+    } else {
+      key[j] = ~K(0);
+      val[j] = 0xffffffffu;
+    }
+  }
+  // warp multisplit: stable rank of each key among equal digits of its warp
+  uint32_t* wh = s_whist + warp * kRadix;
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j) {
+    const int64_t idx = base + (int64_t)warp * 32 * kSortIPT + j * 32 + lane;
+    const bool valid = idx < p.n;
+    const unsigned d = valid ? (unsigned)((key[j] >> shift) & 0xff) : 0x100u;
+    const unsigned peers = __match_any_sync(kFull, d);
+    const int leader = 31 - __clz(peers);
+    uint32_t cnt = 0;
+    if (valid && lane == leader) {
+      cnt = wh[d];
+      wh[d] = cnt + __popc(peers);
+    }
+    cnt = __shfl_sync(kFull, cnt, leader);
+    loc[j] = cnt + __popc(peers & lanemask_lt());
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit (thread == digit): warp-exclusive offsets and the tile count
+  const int d = tid;
+  uint32_t count = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const uint32_t c = s_whist[w * kRadix + d];
+    s_whist[w * kRadix + d] = count;
+    count += c;
+  }
+  // decoupled look-back over preceding tiles of this line
+  unsigned long long* st = p.status + ((int64_t)line * p.tiles) * kRadix;
+  const unsigned long long ep = (unsigned long long)p.epoch << 34;
+  uint32_t excl = 0;
+  if (tile == 0) {
+    atomicExch(&st[d], ep | kFlagPre | count);
+  } else {
+    atomicExch(&st[(int64_t)tile * kRadix + d], ep | kFlagAgg | count);
+    int k = tile - 1;
+    while (true) {
+      const unsigned long long v =
+          *reinterpret_cast<volatile unsigned long long*>(&st[(int64_t)k * kRadix + d]);
+      if ((v >> 34) != p.epoch || ((v >> 32) & 3ull) == 0) continue;
+      excl += (uint32_t)v;
+      if (((v >> 32) & 3ull) == 2) break;
+      --k;
+    }
+    atomicExch(&st[(int64_t)tile * kRadix + d], ep | kFlagPre | (excl + count));
+  }
+  // tile-local exclusive scan of counts over digits
+  uint32_t v = count;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) s_wsum[warp] = v;
+  __syncthreads();
+  uint32_t wofs = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) wofs += (w < warp) ? s_wsum[w] : 0u;
+  const uint32_t start = wofs + v - count;
+  s_start[d] = start;
+  s_gofs[d] = p.bases[(line * p.passes + p.pass) * kRadix + d] + excl - start;
+  __syncthreads();
+  // reorder the tile in shared memory by digit (stable)
+#pragma unroll
+  for (int j = 0; j < kSortIPT; ++j) {
+    const int64_t idx = base + (int64_t)warp * 32 * kSortIPT + j * 32 + lane;
+    if (idx < p.n) {
+      const unsigned dd = (unsigned)((key[j] >> shift) & 0xff);
+      const uint32_t pos = s_start[dd] + s_whist[warp * kRadix + dd] + loc[j];
+      s_keys[pos] = key[j];
+      s_vals[pos] = val[j];
+    }
+  }
+  __syncthreads();
+  // coalesced write-out: runs of equal digits land contiguously
+  const int64_t rem = p.n - base;
+  const int tile_n = rem < kSortTile ? (int)rem : kSortTile;
+  K* kout = reinterpret_cast<K*>(p.dst_keys[line]);
+  uint32_t* vout = p.dst_vals[line];
+  for (int i = tid; i < tile_n; i += kSortThreads) {
+    const K kk = s_keys[i];
+    const unsigned dd = (unsigned)((kk >> shift) & 0xff);
+    const uint32_t g = s_gofs[dd] + (uint32_t)i;
+    if (!LAST) kout[g] = kk;
+    vout[g] = s_vals[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// adjacency
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kBlock) k_neighbors(const uint32_t* __restrict__ p0,
+                                                     const uint32_t* __restrict__ p1,
+                                                     const uint32_t* __restrict__ p2,
+                                                     int64_t n, int2* __restrict__ cand) {
+  const int line = blockIdx.y;
+  const uint32_t* perm = line == 0 ? p0 : (line == 1 ? p1 : p2);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+    const int u = (int)perm[k];
+    const int prev = k > 0 ? (int)perm[k - 1] : -1;
+    const int next = k + 1 < n ? (int)perm[k + 1] : -1;
+    cand[line * n + u] = make_int2(prev, next);
+  }
+}
+
+__device__ __forceinline__ void cswap(unsigned& a, unsigned& b) {
+  const unsigned lo = min(a, b), hi = max(a, b);
+  a = lo;
+  b = hi;
+}
+
+// odd-even transposition sort of 6 values (6 rounds suffice for 6 inputs)
+__device__ __forceinline__ void sort6(unsigned (&c)[6]) {
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    if (r & 1) {
+      cswap(c[1], c[2]);
+      cswap(c[3], c[4]);
+    } else {
+      cswap(c[0], c[1]);
+      cswap(c[2], c[3]);
+      cswap(c[4], c[5]);
+    }
+  }
+}
+
+template <typename K, bool BIG>
+__global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
+                                                 const K* __restrict__ pc, int64_t n, int b,
+                                                 int2* __restrict__ ell,
+                                                 uint32_t* __restrict__ meta,
+                                                 double* __restrict__ partials,
+                                                 Ctl* __restrict__ ctl) {
+  __shared__ double s_red[32 * 2];
+  __shared__ bool s_last;
+  double sg_sum = 0.0, e_cnt = 0.0;
+  int maxdeg = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned c[6];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const int2 v = cand[l * n + i];
+      c[2 * l] = (unsigned)v.x;  // -1 -> 0xffffffff sorts last
+      c[2 * l + 1] = (unsigned)v.y;
+    }
+    sort6(c);
+#pragma unroll
+    for (int s = 5; s > 0; --s)
+      if (c[s] == c[s - 1]) c[s] = 0xffffffffu;
+    sort6(c);
+    int deg = 0;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) deg += (c[s] != 0xffffffffu);
+    long long xi, yi, zi;
+    unpack(pc[i], b, &xi, &yi, &zi);
+    unsigned long long sq[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      sq[s] = ~0ull;
+      if (s < deg) {
+        long long xj, yj, zj;
+        unpack(pc[c[s]], b, &xj, &yj, &zj);
+        const long long dx = xi - xj, dy = yi - yj, dz = zi - zj;
+        sq[s] = (unsigned long long)(dx * dx + dy * dy + dz * dz);
+        if ((int64_t)c[s] > i) {
+          sg_sum += sqrt((double)sq[s]);
+          e_cnt += 1.0;
+        }
+      }
+    }
+    // patch order: rank by (sqdist, index); rows are index-ascending so
+    // the slot number breaks ties exactly like the reference's stable sort
+    uint32_t order = 0;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      int r = 0;
+#pragma unroll
+      for (int t = 0; t < 6; ++t)
+        r += (t < deg) && (sq[t] < sq[s] || (sq[t] == sq[s] && t < s));
+      if (s < deg) order |= (uint32_t)s << (3 * r);
+    }
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const bool ok = s < deg;
+      ell[s * n + i] = make_int2(ok ? (int)c[s] : (int)i,
+                                 (ok && !BIG) ? (int)(uint32_t)sq[s] : 0);
+    }
+    meta[i] = (uint32_t)deg | (order << 3);
+    maxdeg = max(maxdeg, deg);
+  }
+  // block reduce (sum, count) and the max degree
+  maxdeg = __reduce_max_sync(kFull, maxdeg);
+  if ((threadIdx.x & 31) == 0 && maxdeg > 0) atomicMax(&ctl->max_deg, maxdeg);
+  double v[2] = {sg_sum, e_cnt};
+  block_sum<2>(v, s_red);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = v[0];
+    partials[2 * blockIdx.x + 1] = v[1];
+  }
+  if (last_block(&ctl->ticket[0], &s_last)) {
+    double a[2] = {0.0, 0.0};
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+      a[0] += ld_cg(&partials[2 * k]);
+      a[1] += ld_cg(&partials[2 * k + 1]);
+    }
+    block_sum<2>(a, s_red);
+    if (threadIdx.x == 0) {
+      const unsigned long long e = (unsigned long long)a[1];
+      ctl->n_edges = e;
+      ctl->sigma_g = e ? a[0] / (double)e : 0.0;
+      ctl->ticket[0] = 0;
+    }
+  }
+}
+
+// Eq. (4): w = exp(-sqdist / sigma_g^2).  fp64 evaluation, fp32 storage in
+// the slot payload (and fp64 copy in parity mode).
+template <typename K, bool BIG, bool W64>
+__global__ void __launch_bounds__(kBlock) k_weights(int2* __restrict__ ell,
+                                                    double* __restrict__ w64,
+                                                    const K* __restrict__ pc, int64_t n,
+                                                    int b, const Ctl* __restrict__ ctl) {
+  const double sg = ctl->sigma_g;
+  const double sg2 = sg * sg;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    long long xi = 0, yi = 0, zi = 0;
+    if (BIG) unpack(pc[i], b, &xi, &yi, &zi);
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) {
+      int2 sl = ell[s * n + i];
+      double w = 0.0;
+      if (sl.x != (int)i) {
+        unsigned long long sq;
+        if (BIG) {
+          long long xj, yj, zj;
+          unpack(pc[sl.x], b, &xj, &yj, &zj);
+          const long long dx = xi - xj, dy = yi - yj, dz = zi - zj;
+          sq = (unsigned long long)(dx * dx + dy * dy + dz * dz);
+        } else {
+          sq = (uint32_t)sl.y;
+        }
+        w = exp(__ddiv_rn(-(double)sq, sg2));
+      }
+      sl.y = __float_as_int((float)w);
+      ell[s * n + i] = sl;
+      if (W64) w64[s * n + i] = w;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CSR export (reference conventions)
+// ---------------------------------------------------------------------------
+
+__global__ void k_degrees(const uint32_t* __restrict__ meta, const int2* __restrict__ ell,
+                          int64_t n, int64_t* __restrict__ deg, int64_t* __restrict__ updeg) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int dg = (int)(meta[i] & 7u);
+    int up = 0;
+    for (int s = 0; s < dg; ++s) up += (ell[s * n + i].x > (int)i);
+    deg[i] = dg;
+    updeg[i] = up;
+  }
+}
+
+// Exclusive scan, 3 phases (only used by the export path).
+constexpr int kScanTile = 2048;
+__global__ void k_scan_tiles(const int64_t* __restrict__ in, int64_t n,
+                             int64_t* __restrict__ tile_sums) {
+  __shared__ long long s[kBlock / 32];
+  long long acc = 0;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  for (int t = threadIdx.x; t < kScanTile; t += blockDim.x)
+    if (base + t < n) acc += in[base + t];
+  acc = warp_sum_ll(acc);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tot = 0;
+    for (int w = 0; w < kBlock / 32; ++w) tot += s[w];
+    tile_sums[blockIdx.x] = tot;
+  }
+}
+__global__ void k_scan_sums(int64_t* tile_sums, int ntiles, int64_t* total) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    long long run = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const long long v = tile_sums[t];
+      tile_sums[t] = run;
+      run += v;
+    }
+    *total = run;
+  }
+}
+__global__ void k_scan_apply(const int64_t* __restrict__ in, int64_t n,
+                             const int64_t* __restrict__ tile_sums, int64_t* __restrict__ out) {
+  __shared__ long long s[kScanTile];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  for (int t = threadIdx.x; t < kScanTile; t += blockDim.x)
+    s[t] = (base + t < n) ? in[base + t] : 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long run = tile_sums[blockIdx.x];
+    for (int t = 0; t < kScanTile; ++t) {
+      const long long v = s[t];
+      s[t] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kScanTile; t += blockDim.x)
+    if (base + t < n) out[base + t] = s[t];
+}
+
+template <typename K>
+__global__ void k_export(const uint32_t* __restrict__ meta, const int2* __restrict__ ell,
+                         const K* __restrict__ pc, int64_t n, int b,
+                         const int64_t* __restrict__ rowoff, const int64_t* __restrict__ eoff,
+                         const Ctl* __restrict__ ctl, int64_t* __restrict__ indptr,
+                         int64_t* __restrict__ indices, int64_t* __restrict__ csr_edge,
+                         int64_t* __restrict__ edge_u, int64_t* __restrict__ edge_v,
+                         double* __restrict__ sqd, double* __restrict__ wts,
+                         double* __restrict__ wdeg) {
+  const double sg = ctl->sigma_g, sg2 = sg * sg;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int dg = (int)(meta[i] & 7u);
+    const int64_t r0 = rowoff[i];
+    if (indptr) {
+      indptr[i] = r0;
+      if (i == n - 1) indptr[n] = r0 + dg;
+    }
+    long long xi, yi, zi;
+    unpack(pc[i], b, &xi, &yi, &zi);
+    int nlow = 0;
+    double lo = 0.0, hi = 0.0;
+    for (int s = 0; s < dg; ++s) {
+      const int j = ell[s * n + i].x;
+      long long xj, yj, zj;
+      unpack(pc[j], b, &xj, &yj, &zj);
+      const long long dx = xi - xj, dy = yi - yj, dz = zi - zj;
+      const double sq = (double)(unsigned long long)(dx * dx + dy * dy + dz * dz);
+      const double w = exp(__ddiv_rn(-sq, sg2));
+      int64_t eid;
+      if (j > (int)i) {
+        eid = eoff[i] + (s - nlow);
+        if (edge_u) edge_u[eid] = i;
+        if (edge_v) edge_v[eid] = j;
+        if (sqd) sqd[eid] = sq;
+        if (wts) wts[eid] = w;
+        hi += w;
+      } else {
+        ++nlow;
+        const int dj = (int)(meta[j] & 7u);
+        int cnt = 0;
+        for (int t = 0; t < dj; ++t) {
+          const int v = ell[t * n + j].x;
+          cnt += (v > j) && (v < (int)i);
+        }
+        eid = eoff[j] + cnt;
+        lo += w;
+      }
+      if (indices) indices[r0 + s] = j;
+      if (csr_edge) csr_edge[r0 + s] = eid;
+    }
+    if (wdeg) wdeg[i] = hi + lo;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+
+static int grid_for(int64_t n, int cap) {
+  int64_t g = (n + kBlock - 1) / kBlock;
+  if (g < 1) g = 1;
+  return (int)std::min<int64_t>(g, cap);
+}
+
+template <typename K>
+static size_t onesweep_smem() {
+  return (size_t)kSortTile * (sizeof(K) + sizeof(uint32_t)) + 8 * kRadix * sizeof(uint32_t);
+}
+
+template <typename K, bool FIRST, bool LAST, bool SLG>
+static int launch_pass(fgbd_ctx* ctx, SortPass& p, int nlines) {
+  const size_t smem = onesweep_smem<K>();
+  FGBD_CUDA(ctx, cudaFuncSetAttribute(k_onesweep<K, FIRST, LAST, SLG>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(p.tiles, nlines);
+  k_onesweep<K, FIRST, LAST, SLG><<<grid, kSortThreads, smem, ctx->stream>>>(p);
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+// Run `passes` onesweep passes over nlines lines.  On return ctx->perm[l]
+// points at the final permutation of line l.
+template <typename K, bool SLG>
+static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
+                    const K* keys_in) {
+  SortScratch& S = ctx->sort;
+  const int tiles = (int)((n + kSortTile - 1) / kSortTile);
+  const int nh = nlines * passes * kRadix;
+  FGBD_CUDA(ctx, cudaMemsetAsync(S.hist, 0, nh * sizeof(uint32_t), ctx->stream));
+  FGBD_CUDA(ctx, cudaMemsetAsync(S.tile_ctr, 0, kMaxPasses * 3 * sizeof(unsigned), ctx->stream));
+  {
+    const size_t smem = nh * sizeof(uint32_t);
+    const int grid = grid_for(n, ctx->num_sms * 2);
+    if (SLG) {
+      k_prep<K, true><<<grid, kBlock, smem, ctx->stream>>>(
+          ctx->cur_coords, nullptr, n, b, nlines, passes, (K*)ctx->pc, S.hist, ctx->ctl);
+    } else {
+      k_prep<K, false><<<grid, kBlock, smem, ctx->stream>>>(
+          nullptr, keys_in, n, b, nlines, passes, nullptr, S.hist, ctx->ctl);
+    }
+    FGBD_LAUNCH(ctx);
+  }
+  k_scan_hist<<<1, kRadix, 0, ctx->stream>>>(S.hist, nlines * passes);
+  FGBD_LAUNCH(ctx);
+  for (int pass = 0; pass < passes; ++pass) {
+    SortPass p{};
+    for (int l = 0; l < nlines; ++l) {
+      p.src_keys[l] = pass == 0 ? (const void*)keys_in : S.keys[(pass - 1) & 1][l];
+      p.src_vals[l] = pass == 0 ? nullptr : S.vals[(pass - 1) & 1][l];
+      p.dst_keys[l] = S.keys[pass & 1][l];
+      p.dst_vals[l] = S.vals[pass & 1][l];
+    }
+    p.pc = ctx->pc;
+    p.bases = S.hist;
+    p.status = S.status;
+    p.tile_ctr = S.tile_ctr + pass * 3;
+    p.n = n;
+    p.b = b;
+    p.pass = pass;
+    p.passes = passes;
+    p.tiles = tiles;
+    p.epoch = (++S.epoch) & 0x3fffffffu;
+    if (p.epoch == 0) p.epoch = S.epoch = 1;
+    const bool first = pass == 0, last = pass == passes - 1;
+    int rc;
+    if (first && last) rc = launch_pass<K, true, true, SLG>(ctx, p, nlines);
+    else if (first) rc = launch_pass<K, true, false, SLG>(ctx, p, nlines);
+    else if (last) rc = launch_pass<K, false, true, SLG>(ctx, p, nlines);
+    else rc = launch_pass<K, false, false, SLG>(ctx, p, nlines);
+    if (rc) return rc;
+  }
+  for (int l = 0; l < nlines; ++l) ctx->perm[l] = S.vals[(passes - 1) & 1][l];
+  return FGBD_OK;
+}
+
+template <typename K>
+static int graph_impl(fgbd_ctx* ctx, int64_t n, int b) {
+  const int passes = (3 * b + 7) / 8;
+  int rc = run_sort<K, true>(ctx, n, b, 3, passes, nullptr);
+  if (rc) return rc;
+  {
+    dim3 grid(grid_for(n, 1 << 20), 3);
+    k_neighbors<<<grid, kBlock, 0, ctx->stream>>>(ctx->perm[0], ctx->perm[1], ctx->perm[2], n,
+                                                  ctx->cand);
+    FGBD_LAUNCH(ctx);
+  }
+  const int grid = grid_for(n, kRedGrid);
+  if (b > 15) {
+    k_rows<K, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b,
+                                                      ctx->ell, ctx->meta, ctx->partials,
+                                                      ctx->ctl);
+  } else {
+    k_rows<K, false><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b,
+                                                       ctx->ell, ctx->meta, ctx->partials,
+                                                       ctx->ctl);
+  }
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+int launch_graph(fgbd_ctx* ctx, int64_t n, int bits) {
+  int rc = (3 * bits <= 32) ? graph_impl<uint32_t>(ctx, n, bits)
+                            : graph_impl<unsigned long long>(ctx, n, bits);
+  if (rc) return rc;
+  ctx->g_n = n;
+  ctx->g_bits = bits;
+  ctx->g_have_weights = 0;
+  ctx->g_have_noise = 0;
+  return FGBD_OK;
+}
+
+template <typename K>
+static int weights_impl(fgbd_ctx* ctx, int64_t n, int b, int w64) {
+  const int grid = grid_for(n, ctx->num_sms * 8);
+  const K* pc = (const K*)ctx->pc;
+  if (b > 15) {
+    if (w64)
+      k_weights<K, true, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->ell, ctx->w64, pc, n, b, ctx->ctl);
+    else
+      k_weights<K, true, false><<<grid, kBlock, 0, ctx->stream>>>(ctx->ell, ctx->w64, pc, n, b, ctx->ctl);
+  } else {
+    if (w64)
+      k_weights<K, false, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->ell, ctx->w64, pc, n, b, ctx->ctl);
+    else
+      k_weights<K, false, false><<<grid, kBlock, 0, ctx->stream>>>(ctx->ell, ctx->w64, pc, n, b, ctx->ctl);
+  }
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+int launch_weights(fgbd_ctx* ctx, int64_t n, int bits, int w64) {
+  if (w64) {
+    int rc = ensure_w64(ctx, n);
+    if (rc) return rc;
+  }
+  int rc = (3 * bits <= 32) ? weights_impl<uint32_t>(ctx, n, bits, w64)
+                            : weights_impl<unsigned long long>(ctx, n, bits, w64);
+  if (rc) return rc;
+  ctx->g_have_weights = 1;
+  ctx->g_weights64 = w64;
+  return FGBD_OK;
+}
+
+int launch_argsort64(fgbd_ctx* ctx, const uint64_t* d_keys, int64_t n, int key_bits,
+                     uint32_t** d_perm_out) {
+  const int passes = (key_bits + 7) / 8;
+  int rc = run_sort<unsigned long long, false>(ctx, n, 0, 1, passes,
+                                               (const unsigned long long*)d_keys);
+  if (rc) return rc;
+  *d_perm_out = ctx->perm[0];
+  return FGBD_OK;
+}
+
+template <typename K>
+__global__ void k_codes(const K* __restrict__ pc, int64_t n, int b, int line,
+                        uint64_t* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = (uint64_t)line_key(pc[i], line, b);
+}
+
+int launch_scan_line(fgbd_ctx* ctx, int64_t n, int bits, int line, uint64_t* d_codes,
+                     uint32_t** d_perm_out) {
+  const int passes = (3 * bits + 7) / 8;
+  int rc = (3 * bits <= 32) ? run_sort<uint32_t, true>(ctx, n, bits, 3, passes, nullptr)
+                            : run_sort<unsigned long long, true>(ctx, n, bits, 3, passes, nullptr);
+  if (rc) return rc;
+  if (d_codes) {
+    const int grid = grid_for(n, ctx->num_sms * 8);
+    if (3 * bits <= 32)
+      k_codes<uint32_t><<<grid, kBlock, 0, ctx->stream>>>((const uint32_t*)ctx->pc, n, bits,
+                                                         line, d_codes);
+    else
+      k_codes<unsigned long long><<<grid, kBlock, 0, ctx->stream>>>(
+          (const unsigned long long*)ctx->pc, n, bits, line, d_codes);
+    FGBD_LAUNCH(ctx);
+  }
+  *d_perm_out = ctx->perm[line];
+  return FGBD_OK;
+}
+
+int scan_exclusive(fgbd_ctx* ctx, const int64_t* in, int64_t n, int64_t* out,
+                          int64_t* tmp, int64_t* d_total) {
+  const int tiles = (int)((n + kScanTile - 1) / kScanTile);
+  k_scan_tiles<<<tiles, kBlock, 0, ctx->stream>>>(in, n, tmp);
+  FGBD_LAUNCH(ctx);
+  k_scan_sums<<<1, 32, 0, ctx->stream>>>(tmp, tiles, d_total);
+  FGBD_LAUNCH(ctx);
+  k_scan_apply<<<tiles, kBlock, 0, ctx->stream>>>(in, n, tmp, out);
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+int launch_export(fgbd_ctx* ctx, int64_t n, int64_t* d_indptr, int64_t* d_indices,
+                  int64_t* d_csr_edge, int64_t* d_edge_u, int64_t* d_edge_v, double* d_sqdist,
+                  double* d_weights, double* d_wdeg, int64_t* nnz_out, int64_t* e_out) {
+  // scratch: deg, updeg, rowoff, eoff (4n) + tile sums + 2 totals
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  const size_t need = (size_t)(4 * n + 2 * tiles + 2) * sizeof(int64_t);
+  if (ctx->csr_scratch_bytes < need) {
+    if (ctx->csr_scratch) cudaFree(ctx->csr_scratch);
+    ctx->csr_scratch = nullptr;
+    FGBD_CUDA(ctx, cudaMalloc(&ctx->csr_scratch, need));
+    ctx->csr_scratch_bytes = need;
+  }
+  int64_t* deg = (int64_t*)ctx->csr_scratch;
+  int64_t* updeg = deg + n;
+  int64_t* rowoff = updeg + n;
+  int64_t* eoff = rowoff + n;
+  int64_t* t1 = eoff + n;
+  int64_t* t2 = t1 + tiles;
+  int64_t* totals = t2 + tiles;
+  const int grid = grid_for(n, ctx->num_sms * 8);
+  k_degrees<<<grid, kBlock, 0, ctx->stream>>>(ctx->meta, ctx->ell, n, deg, updeg);
+  FGBD_LAUNCH(ctx);
+  int rc = scan_exclusive(ctx, deg, n, rowoff, t1, totals);
+  if (rc) return rc;
+  rc = scan_exclusive(ctx, updeg, n, eoff, t2, totals + 1);
+  if (rc) return rc;
+  if (3 * ctx->g_bits <= 32)
+    k_export<uint32_t><<<grid, kBlock, 0, ctx->stream>>>(
+        ctx->meta, ctx->ell, (const uint32_t*)ctx->pc, n, ctx->g_bits, rowoff, eoff, ctx->ctl,
+        d_indptr, d_indices, d_csr_edge, d_edge_u, d_edge_v, d_sqdist, d_weights, d_wdeg);
+  else
+    k_export<unsigned long long><<<grid, kBlock, 0, ctx->stream>>>(
+        ctx->meta, ctx->ell, (const unsigned long long*)ctx->pc, n, ctx->g_bits, rowoff, eoff,
+        ctx->ctl, d_indptr, d_indices, d_csr_edge, d_edge_u, d_edge_v, d_sqdist, d_weights,
+        d_wdeg);
+  FGBD_LAUNCH(ctx);
+  int64_t h[2];
+  FGBD_CUDA(ctx, cudaMemcpyAsync(h, totals, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *nnz_out = h[0];
+  *e_out = h[1];
+  return FGBD_OK;
+}
+
+}  // namespace fgbd

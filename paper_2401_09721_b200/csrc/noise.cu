@@ -1,0 +1,325 @@
+// NE-GBP noise estimation (reference noise.py:82-249) and the FSLR
+// statistic (filtering.py:186).
+//
+// Device: one pass over the eligible points.  Block = 3 warps, warp c owns
+// colour channel c, lane = point.  Each thread assembles its point's patch
+// (own value, then the D-1 nearest neighbours in (sqdist, index) order,
+// precomputed by k_rows) and accumulates shifted one-pass moments
+// sum(a_k - 128) and sum((a_k - 128)(a_l - 128)) in fp64.  The per-point
+// FSLR statistic mean_c std_c(patch) is computed with numpy's exact
+// evaluation order (left-to-right sums, no FMA) so the mask is bit-exact.
+// Block partials are reduced in a fixed order by k_reduce_cols.
+//
+// Host: covariance from the moments, cyclic Jacobi (noise.py:133-185) and
+// the tail rule (noise.py:188-216) -- a 7x7 problem per channel.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+#include "device_util.cuh"
+#include "fgbd_internal.cuh"
+
+namespace fgbd {
+
+constexpr int kNeThreads = 96;
+constexpr int kNeVals = 3 * kMom + 1;  // moments + eligible count
+
+__device__ __forceinline__ int mom2_index(int k, int l) {  // k <= l, D = 7 layout
+  return 7 + k * 7 - (k * (k - 1)) / 2 + (l - k);
+}
+
+__global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict__ meta,
+                                                      const int2* __restrict__ ell,
+                                                      const double* __restrict__ colors,
+                                                      int64_t n, int D,
+                                                      double* __restrict__ fslr,
+                                                      double* __restrict__ part /*[vals][grid]*/) {
+  __shared__ double s_std[3][32];
+  const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double m[kMom];
+#pragma unroll
+  for (int k = 0; k < kMom; ++k) m[k] = 0.0;
+  long long elig = 0;
+  const double invD = 0.0;  // unused; divisions below are exact __ddiv_rn
+  (void)invD;
+  const int64_t nchunks = (n + 31) / 32;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t i = ch * 32 + lane;
+    const bool valid = i < n;
+    const uint32_t mt = valid ? meta[i] : 0u;
+    const int deg = (int)(mt & 7u);
+    const bool ok = valid && deg >= D - 1;
+    double a[7];
+#pragma unroll
+    for (int r = 0; r < 7; ++r) a[r] = 0.0;
+    double sd = 0.0;
+    if (ok) {
+      a[0] = colors[3 * i + c];
+#pragma unroll
+      for (int r = 1; r < 7; ++r) {
+        if (r < D) {
+          const int s = (int)((mt >> (3 + 3 * (r - 1))) & 7u);
+          const int j = ell[s * n + i].x;
+          a[r] = colors[3 * (int64_t)j + c];
+        }
+      }
+      // shifted one-pass moments (only the first D entries are non-zero)
+      double v[7];
+#pragma unroll
+      for (int k = 0; k < 7; ++k) v[k] = (k < D) ? a[k] - 128.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        m[k] += v[k];
+#pragma unroll
+        for (int l = k; l < 7; ++l) m[mom2_index(k, l)] = fma(v[k], v[l], m[mom2_index(k, l)]);
+      }
+      // numpy std over the patch axis: sequential sum, /D, squared
+      // deviations, sequential sum, /D, sqrt -- no contraction.
+      double s = a[0];
+#pragma unroll
+      for (int k = 1; k < 7; ++k)
+        if (k < D) s = __dadd_rn(s, a[k]);
+      const double mean = __ddiv_rn(s, (double)D);
+      double var = 0.0;
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        if (k < D) {
+          const double dv = __dadd_rn(a[k], -mean);
+          var = __dadd_rn(var, __dmul_rn(dv, dv));
+        }
+      }
+      sd = __dsqrt_rn(__ddiv_rn(var, (double)D));
+    }
+    s_std[c][lane] = sd;
+    __syncthreads();
+    if (c == 0 && valid) {
+      fslr[i] = ok ? __ddiv_rn(__dadd_rn(__dadd_rn(s_std[0][lane], s_std[1][lane]),
+                                         s_std[2][lane]),
+                               3.0)
+                   : -1.0;
+      elig += ok;
+    }
+    __syncthreads();
+  }
+  // per-warp (= per-channel) reduction, fixed tree
+#pragma unroll
+  for (int k = 0; k < kMom; ++k) {
+    const double t = warp_sum(m[k]);
+    if (lane == 0) part[(int64_t)(c * kMom + k) * gridDim.x + blockIdx.x] = t;
+  }
+  if (c == 0) {
+    const long long e = warp_sum_ll(elig);
+    if (lane == 0) part[(int64_t)(3 * kMom) * gridDim.x + blockIdx.x] = (double)e;
+  }
+}
+
+// out[v] = sum_b part[v][b] in a fixed tree (one block per value).
+__global__ void __launch_bounds__(kBlock) k_reduce_cols(const double* __restrict__ part,
+                                                        int nblocks, Ctl* __restrict__ ctl) {
+  __shared__ double s_red[32];
+  const int v = blockIdx.x;
+  double a[1] = {0.0};
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) a[0] += part[(int64_t)v * nblocks + b];
+  block_sum<1>(a, s_red);
+  if (threadIdx.x == 0) {
+    if (v < 3 * kMom) ctl->mom[v / kMom][v % kMom] = a[0];
+    else ctl->eligible = (long long)a[0];
+  }
+}
+
+int launch_noise(fgbd_ctx* ctx, int64_t n, int patch) {
+  const int64_t nchunks = (n + 31) / 32;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, kNeGrid));
+  k_noise<<<grid, kNeThreads, 0, ctx->stream>>>(ctx->meta, ctx->ell, ctx->buf[BUF_Y], n, patch,
+                                                ctx->fslr, ctx->partials);
+  FGBD_LAUNCH(ctx);
+  k_reduce_cols<<<kNeVals, kBlock, 0, ctx->stream>>>(ctx->partials, grid, ctx->ctl);
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host: Jacobi + tail rule
+// ---------------------------------------------------------------------------
+
+static double np_sign(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
+
+int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err) {
+  // symmetry check on the raw input (noise.py:142-144)
+  double scale = 0.0, asym = 0.0;
+  for (int i = 0; i < d * d; ++i) scale = std::max(scale, std::fabs(s[i]));
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) asym = std::max(asym, std::fabs(s[i * d + j] - s[j * d + i]));
+  if (scale > 0 && asym > 1e-9 * scale) {
+    *err = "matrix is not symmetric within tolerance";
+    return FGBD_E_NOISE;
+  }
+  std::vector<double> a(d * d);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) a[i * d + j] = (s[i * d + j] + s[j * d + i]) * 0.5;
+  auto finish = [&]() {
+    for (int i = 0; i < d; ++i) out_desc[i] = a[i * d + i];
+    std::sort(out_desc, out_desc + d, [](double x, double y) { return x > y; });
+  };
+  double fro2 = 0.0;
+  for (int i = 0; i < d * d; ++i) fro2 += a[i] * a[i];
+  const double norm = std::sqrt(fro2);
+  if (norm == 0.0 || d == 1) {
+    finish();
+    return FGBD_OK;
+  }
+  const double target = 1e-12 * norm;
+  auto off_norm = [&]() {
+    double all = 0.0, dg = 0.0;
+    for (int i = 0; i < d * d; ++i) all += a[i] * a[i];
+    for (int i = 0; i < d; ++i) dg += a[i * d + i] * a[i * d + i];
+    return std::sqrt(std::max(all - dg, 0.0));
+  };
+  std::vector<double> cp(d), cq(d);
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    if (off_norm() <= target) {
+      finish();
+      return FGBD_OK;
+    }
+    for (int p = 0; p < d - 1; ++p) {
+      for (int q = p + 1; q < d; ++q) {
+        const double apq = a[p * d + q];
+        if (apq == 0.0) continue;
+        const double diff = a[q * d + q] - a[p * d + p];
+        double t;
+        if (std::fabs(apq) < 1e-36 * std::fabs(diff)) {
+          t = apq / diff;
+        } else {
+          const double theta = diff / (2.0 * apq);
+          t = np_sign(theta) / (std::fabs(theta) + std::hypot(theta, 1.0));
+          if (t == 0.0) t = 1.0;
+        }
+        const double c = 1.0 / std::sqrt(t * t + 1.0);
+        const double sn = t * c;
+        for (int i = 0; i < d; ++i) {
+          cp[i] = a[i * d + p];
+          cq[i] = a[i * d + q];
+        }
+        for (int i = 0; i < d; ++i) {
+          a[i * d + p] = c * cp[i] - sn * cq[i];
+          a[i * d + q] = sn * cp[i] + c * cq[i];
+        }
+        for (int j = 0; j < d; ++j) {
+          cp[j] = a[p * d + j];
+          cq[j] = a[q * d + j];
+        }
+        for (int j = 0; j < d; ++j) {
+          a[p * d + j] = c * cp[j] - sn * cq[j];
+          a[q * d + j] = sn * cp[j] + c * cq[j];
+        }
+        a[p * d + q] = 0.0;
+        a[q * d + p] = 0.0;
+      }
+    }
+  }
+  const double off = off_norm();
+  if (off <= target) {
+    finish();
+    return FGBD_OK;
+  }
+  char buf[128];
+  std::snprintf(buf, sizeof(buf), "Jacobi did not converge in 50 sweeps (off-diagonal %.3e)", off);
+  *err = buf;
+  return FGBD_E_NOISE;
+}
+
+static double median_of(const double* v, int m) {
+  std::vector<double> s(v, v + m);
+  std::sort(s.begin(), s.end());
+  if (m & 1) return s[m / 2];
+  return (s[m / 2 - 1] + s[m / 2]) / 2.0;
+}
+
+int select_tail_host(const double* lam, int d, int divisor, int* m_out, double* tau_out,
+                     int* fb_out, std::string* err) {
+  if (d < 3) {
+    *err = "need at least 3 eigenvalues, got " + std::to_string(d);
+    return FGBD_E_NOISE;
+  }
+  double scale = 1.0;
+  for (int i = 0; i < d; ++i) scale = std::max(scale, std::fabs(lam[i]));
+  for (int i = 0; i + 1 < d; ++i)
+    if (lam[i + 1] - lam[i] > 1e-9 * scale) {
+      *err = "eigenvalues must be sorted descending";
+      return FGBD_E_NOISE;
+    }
+  if (divisor != FGBD_TAU_COUNT && divisor != FGBD_TAU_COUNT_PLUS_ONE) {
+    *err = "unknown divisor rule";
+    return FGBD_E_NOISE;
+  }
+  const int extra = divisor == FGBD_TAU_COUNT ? 0 : 1;
+  auto tail_tau = [&](int m) {
+    double s = 0.0;
+    for (int k = m; k < d; ++k) s += lam[k];  // numpy sum of <8 values: sequential
+    return s / (double)(d - m + extra);
+  };
+  for (int m = 1; m < d - 1; ++m) {
+    const double tau = tail_tau(m);
+    if (tau > median_of(lam + m, d - m)) {
+      *m_out = m;
+      *tau_out = tau;
+      *fb_out = 0;
+      return FGBD_OK;
+    }
+  }
+  const int m = d / 2;
+  *m_out = m;
+  *tau_out = tail_tau(m);
+  *fb_out = 1;
+  return FGBD_OK;
+}
+
+// Reads the reduced moments (ctl mirror must be current) and finishes
+// noise.py:122-243 on the host.
+int finish_noise(fgbd_ctx* ctx, int D, int divisor, fgbd_noise* out) {
+  const Ctl& h = *ctx->ctl_host;
+  std::memset(out, 0, sizeof(*out));
+  out->patch_size = D;
+  const long long ne = h.eligible;
+  out->eligible_count = ne;
+  if (ne < 2)
+    return set_error(ctx, FGBD_E_NOISE, "need at least 2 patches, have " + std::to_string(ne));
+  double sig[3];
+  for (int c = 0; c < 3; ++c) {
+    const double* s1 = h.mom[c];
+    double mu[7];
+    for (int k = 0; k < D; ++k) mu[k] = s1[k] / (double)ne;
+    double cov[7 * 7];
+    for (int k = 0; k < D; ++k) {
+      for (int l = k; l < D; ++l) {
+        const int idx = 7 + k * 7 - (k * (k - 1)) / 2 + (l - k);
+        const double v = h.mom[c][idx] / (double)ne - mu[k] * mu[l];
+        cov[k * D + l] = v;
+        cov[l * D + k] = v;
+      }
+    }
+    for (int k = 0; k < D; ++k)
+      for (int l = 0; l < D; ++l) out->covariance[c][k][l] = cov[k * D + l];
+    std::string err;
+    double lam[7];
+    int rc = jacobi_eigenvalues(cov, D, lam, &err);
+    if (rc) return set_error(ctx, rc, err);
+    int m, fb;
+    double tau;
+    rc = select_tail_host(lam, D, divisor, &m, &tau, &fb, &err);
+    if (rc) return set_error(ctx, rc, err);
+    for (int k = 0; k < D; ++k) out->eigenvalues[c][k] = lam[k];
+    out->m[c] = m;
+    out->tau[c] = tau;
+    out->fallback[c] = fb;
+    sig[c] = std::sqrt(std::max(tau, 0.0));
+    out->per_channel_sigma[c] = sig[c];
+  }
+  out->sigma_est = ((sig[0] + sig[1]) + sig[2]) / 3.0;
+  return FGBD_OK;
+}
+
+}  // namespace fgbd

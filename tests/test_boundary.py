@@ -1,0 +1,180 @@
+"""CPU suite: the drop-in boundary without a GPU.
+
+- the C-ABI library loads and exports every symbol include/fgbd_b200.h declares;
+- the host-side C++ pieces (Jacobi, tail rule) agree with the reference's
+  frozen eigen data and the SPEC examples;
+- the Python boundary mirrors the reference's types, defaults and errors;
+- device entry points fail loudly (DeviceError) when no GPU is present.
+"""
+
+from __future__ import annotations
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2401_09721_b200 as fb
+from conftest import ROOT, golden_index
+from paper_2401_09721_b200 import _native
+
+HEADER = ROOT / "include" / "fgbd_b200.h"
+
+
+def header_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(fgbd_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _native.load_library()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), f"{s} declared in fgbd_b200.h but not exported"
+    assert sorted(_native.EXPORTED) == syms
+    assert lib.fgbd_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    lib = _native.LIB_PATH
+    data = lib.read_bytes()
+    assert b"sm_100a" in data or b"sm_100" in data
+
+
+def test_ctypes_structs_match_header_layout():
+    # sizes of the mirrored structs must match the C compiler's layout
+    import ctypes
+    import subprocess
+    import tempfile
+
+    src = f"""
+#include <stdio.h>
+#include "{HEADER}"
+int main() {{ printf("%zu %zu %zu %zu\\n", sizeof(fgbd_config), sizeof(fgbd_report),
+                     sizeof(fgbd_noise), sizeof(fgbd_graph_info)); return 0; }}
+"""
+    with tempfile.TemporaryDirectory() as d:
+        c = Path(d) / "s.c"
+        c.write_text(src)
+        exe = Path(d) / "s"
+        subprocess.run(["gcc", str(c), "-o", str(exe)], check=True)
+        sizes = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                  check=True).stdout.split()]
+    assert sizes == [ctypes.sizeof(_native.Config), ctypes.sizeof(_native.Report),
+                     ctypes.sizeof(_native.Noise), ctypes.sizeof(_native.GraphInfo)]
+
+
+def test_host_jacobi_matches_reference_eigenvalues():
+    """fgbd_symmetric_eigenvalues on the reference's own covariance matrices."""
+    n = 0
+    for name, rec in golden_index().items():
+        nz = rec.get("noise")
+        if not nz:
+            continue
+        for c in range(3):
+            cov = np.array(nz["covariance"][c])
+            lam = fb.symmetric_eigenvalues(cov)
+            ref = np.array(nz["eigenvalues"][c])
+            scale = max(1.0, float(np.abs(ref).max()))
+            assert np.max(np.abs(lam - ref)) <= 1e-12 * scale, name
+            sel = fb.select_tail(ref, rec["cfg"]["tau_divisor"])
+            assert sel.m == nz["m"][c] and sel.fallback == nz["fallback"][c]
+            assert sel.tau == pytest.approx(nz["tau"][c], rel=1e-15, abs=1e-300)
+            n += 1
+    assert n > 50
+
+
+def test_host_jacobi_spec_examples():
+    assert fb.symmetric_eigenvalues(np.diag([2.0, 1.0])).tolist() == [2.0, 1.0]
+    assert fb.symmetric_eigenvalues(np.ones((2, 2))) == pytest.approx([2.0, 0.0], abs=1e-12)
+    with pytest.raises(fb.NoiseEstimationError, match="not symmetric"):
+        fb.symmetric_eigenvalues(np.array([[1.0, 2.0], [0.0, 1.0]]))
+    rng = np.random.default_rng(3)
+    for _ in range(100):
+        a = rng.standard_normal((7, 7))
+        s = (a + a.T) / 2
+        lam = fb.symmetric_eigenvalues(s)
+        assert lam.sum() == pytest.approx(np.trace(s), rel=1e-9, abs=1e-9)
+        assert np.allclose(lam, np.sort(np.linalg.eigvalsh(s))[::-1], atol=1e-10)
+    t = fb.select_tail(np.array([50, 2.0, 1.0, 0.9, 0.8, 0.7, 0.6]))
+    assert (t.m, t.fallback) == (1, False) and t.tau == pytest.approx(1.0)
+    t = fb.select_tail(np.full(7, 4.0))
+    assert (t.m, t.tau, t.fallback) == (3, 4.0, True)
+    with pytest.raises(fb.NoiseEstimationError, match="at least 3 eigenvalues"):
+        fb.select_tail(np.array([1.0, 0.5]))
+
+
+def test_filter_config_validation_matches_reference():
+    with pytest.raises(fb.FilterError, match="q_max must be >= 0"):
+        fb.FilterConfig(q_max=-1)
+    with pytest.raises(fb.FilterError, match="reestimate_interval"):
+        fb.FilterConfig(reestimate_interval=0)
+    with pytest.raises(fb.FilterError, match="patch_size must be >= 2"):
+        fb.FilterConfig(patch_size=1)
+    with pytest.raises(fb.FilterError, match="criterion_mode"):
+        fb.FilterConfig(criterion_mode="max")
+    c = fb.FilterConfig()
+    assert (c.q_max, c.epsilon, c.fslr_enabled, c.patch_size, c.reestimate_interval,
+            c.fslr_sigma_floor, c.criterion_mode, c.early_exit, c.tau_divisor) == \
+        (64, None, True, 7, 10, 0.5, "pooled", True, "count")
+    assert issubclass(fb.AllPointsExcludedError, fb.FilterError)
+    for e in (fb.CloudError, fb.GraphError, fb.NoiseEstimationError, fb.FilterError):
+        assert issubclass(e, ValueError)
+
+
+def test_point_cloud_contract():
+    with pytest.raises(fb.CloudError, match=r"coords must be \(N, 3\)"):
+        fb.PointCloud(np.zeros((3, 2)), np.zeros((3, 2)))
+    with pytest.raises(fb.CloudError, match="colors must lie in"):
+        fb.PointCloud(np.zeros((1, 3), np.int64), np.full((1, 3), 256.0), 1)
+    with pytest.raises(fb.CloudError, match="out of range"):
+        fb.PointCloud(np.full((1, 3), 2, np.int64), np.zeros((1, 3)), 1)
+    with pytest.raises(fb.CloudError, match="at least one point"):
+        fb.PointCloud(np.zeros((0, 3), np.int64), np.zeros((0, 3)), 1)
+    pc = fb.PointCloud(np.zeros((2, 3), np.int64), np.zeros((2, 3)), 3)
+    assert not pc.coords.flags.writeable and not pc.colors.flags.writeable
+    assert pc.coords.dtype == np.int64 and pc.colors.dtype == np.float64
+    assert fb.infer_bit_depth(np.array([[0, 5, 1]])) == 3
+
+
+def test_denoise_host_paths_need_no_gpu():
+    one = fb.PointCloud(np.zeros((1, 3), np.int64), np.full((1, 3), 9.0), 1)
+    out, rep = fb.denoise(one)
+    assert out is one and rep.selected_q == 0 and rep.sigma_est == 0.0
+    assert rep.to_dict() == {"selected_q": 0, "sigma_est": 0.0, "masked_fraction": 0.0,
+                             "stage_timings": {"graph_construction": 0.0,
+                                               "noise_estimation": 0.0,
+                                               "low_pass_filter": 0.0},
+                             "cached": False}
+    fl = fb.PointCloud(np.zeros((4, 3)), np.zeros((4, 3)))
+    with pytest.raises(fb.GraphError, match="integer voxel coordinates"):
+        fb.denoise(fl)
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    pc, _ = fb.generate_cloud("ramp", 1000)
+    with pytest.raises(fb.DeviceError):
+        fb.denoise(pc)
+
+
+def test_report_to_dict_shape():
+    r = fb.DenoiseReport(selected_q=3, sigma_est=1.5, masked_fraction=0.25,
+                         criterion_value=0.1, converged=False, eligible_count=10,
+                         device={"steps": 6})
+    d = r.to_dict()
+    assert list(d) == ["selected_q", "sigma_est", "masked_fraction", "stage_timings", "cached",
+                       "criterion_value", "converged", "eligible_count"]
+    assert "device" not in d
+
+
+def test_product_package_never_imports_oracle():
+    pkg = ROOT / "paper_2401_09721_b200"
+    for f in pkg.rglob("*.py"):
+        text = f.read_text()
+        assert not re.search(r"^\s*(import|from)\s+oracle|fgbd_oracle", text, re.M), f

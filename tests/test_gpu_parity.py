@@ -1,0 +1,266 @@
+"""GPU suite: the CUDA path against the reference's frozen outputs and the oracle.
+
+Bars (north_star / SURVEY.md section 8):
+  * radix permutations, CSR structure, edge list, FSLR mask, q and the number
+    of filter steps S: bit-exact;
+  * the filter arithmetic with injected fp64 weights: bit-exact;
+  * sigma_est: 1e-10 relative (north star allows 1e-5);
+  * sigma_g: 1e-12 relative (pairwise vs tree summation order);
+  * colours: 1e-4 absolute on the [0, 1] scale (0.0255 on [0, 255]);
+  * PSNR vs the clean cloud: within 0.01 dB of the reference's.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2401_09721_b200 as fb
+from conftest import cfg_kwargs, custom_input, digest, golden_case, golden_names, regen_input
+from oracle import fgbd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+COLOR_ATOL = 1e-4 * 255.0
+SIGMA_RTOL = 1e-10
+PSNR_TOL = 0.01
+
+
+def _input(name):
+    rec, arr = golden_case(name)
+    if "coords" in arr:
+        return rec, arr, None, custom_input(arr, rec)
+    clean, noisy = regen_input(rec)
+    return rec, arr, clean, noisy
+
+
+def _cfg(rec):
+    c = cfg_kwargs(rec)
+    return fb.FilterConfig(**c) if c else fb.FilterConfig()
+
+
+# ---------------------------------------------------------------------------
+# sort / graph
+# ---------------------------------------------------------------------------
+
+
+def test_radix_argsort_known_answers(gpu_ready):
+    assert fb.radix_argsort(np.array([5, 2, 9], np.uint64)).tolist() == [1, 0, 2]
+    assert fb.radix_argsort(np.full(10000, 3, np.uint64)).tolist() == list(range(10000))
+    assert fb.radix_argsort(np.array([], np.uint64)).tolist() == []
+    assert fb.radix_argsort(np.array([4], np.uint64)).tolist() == [0]
+
+
+@pytest.mark.parametrize("n,bits,dup", [(100_000, 64, 7), (333_333, 21, 3), (4097, 8, 2),
+                                        (4096, 30, 1), (1_000_003, 40, 5), (70_000, 1, 1)])
+def test_radix_argsort_random_equals_stable_argsort(gpu_ready, n, bits, dup):
+    rng = np.random.default_rng(n + bits)
+    hi = np.uint64(2 ** bits - 1) if bits < 64 else np.uint64(2 ** 64 - 1)
+    keys = rng.integers(0, hi, size=n, dtype=np.uint64, endpoint=True)
+    keys[::dup] = keys[0]
+    got = fb.radix_argsort(keys, key_bits=bits)
+    assert np.array_equal(got, np.argsort(keys, kind="stable"))
+    assert np.array_equal(got, O.radix_argsort(keys, bits)) if n <= 100_000 else True
+
+
+FULL = golden_names("s5k_") + golden_names("rand_") + golden_names("tiny_")
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_scan_lines_and_graph_bit_exact(gpu_ready, name):
+    rec, arr, _, pc = _input(name)
+    for line in (1, 2, 3):
+        codes = fb.scanline_codes(pc, line)
+        assert np.array_equal(codes.codes, O.scanline_codes(pc.coords, rec["bit_depth"], line))
+        assert np.array_equal(fb.sort_permutation(codes), arr[f"perm{line}"])
+    g = fb.build_slg(pc)
+    for key in ("indptr", "indices", "csr_edge", "edge_u", "edge_v", "edge_sqdist"):
+        assert np.array_equal(getattr(g, key), arr[key]), key
+    if g.n_edges:
+        gw = fb.build_weighted_slg(pc)
+        assert gw.sigma_g == pytest.approx(rec["graph"]["sigma_g"], rel=1e-12)
+        np.testing.assert_allclose(gw.edge_weights, arr["edge_weights"], rtol=1e-12, atol=0)
+        np.testing.assert_allclose(gw.weighted_degrees(), arr["weighted_degrees"], rtol=1e-12)
+        assert fb.compute_sigma_g(pc, g) == pytest.approx(rec["graph"]["sigma_g"], rel=1e-12)
+
+
+@pytest.mark.parametrize("name", golden_names("m20k_") + golden_names("l100k_") +
+                         golden_names("v20k_"))
+def test_graph_digests_bit_exact(gpu_ready, name):
+    rec, arr, _, pc = _input(name)
+    g = fb.build_slg(pc)
+    gr = rec["graph"]
+    assert g.n_edges == gr["n_edges"]
+    for key in ("indptr", "indices", "csr_edge", "edge_u", "edge_v", "edge_sqdist"):
+        assert digest(getattr(g, key)) == gr[f"sha_{key}"], key
+
+
+# ---------------------------------------------------------------------------
+# filter arithmetic with injected weights: bit-exact against the reference
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", golden_names("s5k_") + ["rand_b4_500", "rand_b3_1000_dups"])
+def test_filter_step_weight_injection_bit_exact(gpu_ready, name):
+    rec, arr, _, pc = _input(name)
+    ref_g = fb.Graph(pc.n_points, arr["indptr"], arr["indices"], arr["csr_edge"], arr["edge_u"],
+                     arr["edge_v"], arr["edge_sqdist"], rec["graph"]["sigma_g"],
+                     arr["edge_weights"])
+    og = O.build_slg(pc.coords, rec["bit_depth"])
+    og.edge_weights = arr["edge_weights"]
+    op = O.EllOperator(og)
+    x = pc.colors
+    for q in (1, 2, 5):
+        want = pc.colors
+        for _ in range(q):
+            want = op.step(want)
+        got = fb.apply_filter(ref_g, x, q)
+        assert np.array_equal(got, want), f"q={q}"
+    assert np.array_equal(fb.filter_step(ref_g, x[:, 0]), op.step(x)[:, 0])
+
+
+def test_filter_two_node_known_answer(gpu_ready):
+    g = fb.build_weighted_slg(fb.PointCloud(np.array([[0, 0, 0], [1, 0, 0]]),
+                                            np.array([[0.0] * 3, [100.0] * 3]), 1))
+    out = fb.filter_step(g, np.array([[0.0, 0, 0], [100.0, 100, 100]]))
+    assert out[:, 0].tolist() == [50.0, 50.0]
+
+
+# ---------------------------------------------------------------------------
+# NE-GBP + FSLR
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", [n for n in golden_names(require=["noise"])
+                                  if not n.startswith("x1m_")])
+def test_noise_estimate(gpu_ready, name):
+    rec, arr, _, pc = _input(name)
+    cfg = _cfg(rec)
+    g = fb.build_weighted_slg(pc)
+    est = fb.estimate_noise(pc, g, cfg.patch_size, cfg.tau_divisor)
+    nz = rec["noise"]
+    assert est.sigma_est == pytest.approx(nz["sigma_est"], rel=SIGMA_RTOL)
+    assert est.eligible_count == nz["eligible_count"]
+    assert est.m.tolist() == nz["m"] and est.fallback.tolist() == nz["fallback"]
+    np.testing.assert_allclose(est.eigenvalues, np.array(nz["eigenvalues"]), rtol=1e-9,
+                               atol=1e-9 * np.abs(nz["eigenvalues"]).max())
+
+
+@pytest.mark.parametrize("name", [n for n in FULL if "patch_vectors" in golden_case(n)[1]])
+def test_patches_and_fslr_stat_bit_exact(gpu_ready, name):
+    rec, arr, _, pc = _input(name)
+    g = fb.build_weighted_slg(pc)
+    ps = fb.extract_patches(pc, g, 7)
+    assert np.array_equal(ps.point_index, arr["patch_point_index"])
+    assert np.array_equal(ps.vectors, arr["patch_vectors"])
+    cov = fb.patch_covariance(ps, 0)
+    np.testing.assert_allclose(cov, np.array(rec["noise"]["covariance"][0]), rtol=1e-10,
+                               atol=1e-10 * np.abs(cov).max())
+    mask = fb.fslr_mask(ps, rec["noise"]["sigma_est"])
+    want = np.ones(pc.n_points, bool)
+    want[arr["patch_point_index"][arr["fslr_stat"] > 2.0 * rec["noise"]["sigma_est"]]] = False
+    assert np.array_equal(mask.include, want)
+
+
+# ---------------------------------------------------------------------------
+# end to end
+# ---------------------------------------------------------------------------
+
+def _check_e2e(rec, arr, clean, out, rep):
+    r = rec["report"]
+    assert rep.selected_q == r["selected_q"]
+    assert rep.cached == r["cached"]
+    if not r["cached"]:
+        assert rep.device["steps"] == rec["steps"]
+        assert rep.sigma_est == pytest.approx(r["sigma_est"], rel=SIGMA_RTOL)
+        assert rep.masked_fraction == r["masked_fraction"]
+        assert rep.eligible_count == r["eligible_count"]
+        assert rep.converged == r["converged"]
+        assert rep.criterion_value == pytest.approx(r["criterion_value"], rel=1e-6, abs=1e-8)
+        np.testing.assert_allclose(rep.device["trace"], rec["trace"], rtol=1e-6, atol=1e-8)
+    else:
+        assert rep.sigma_est == r["sigma_est"]
+    if "out_colors" in arr:
+        assert np.max(np.abs(out.colors - arr["out_colors"])) <= COLOR_ATOL
+    if "out_colors_f32" in arr:
+        assert np.max(np.abs(out.colors - arr["out_colors_f32"])) <= COLOR_ATOL
+    if clean is not None and "psnr_out" in rec:
+        assert abs(fb.psnr(clean, out) - rec["psnr_out"]) <= PSNR_TOL
+    assert out.colors.min() >= 0.0 and out.colors.max() <= 255.0
+    np.testing.assert_array_equal(out.coords, out.coords)
+
+
+E2E = [n for n in golden_names(require=["report"]) if not n.startswith(("x1m_", "checker"))]
+
+
+@pytest.mark.parametrize("name", E2E)
+def test_denoise_matches_reference(gpu_ready, name):
+    rec, arr, clean, pc = _input(name)
+    out, rep = fb.denoise(pc, _cfg(rec), cached_q=rec.get("cached_q"),
+                          cached_sigma_est=rec.get("cached_sigma"))
+    _check_e2e(rec, arr, clean, out, rep)
+
+
+@pytest.mark.parametrize("name", golden_names(require=["denoise_error"]))
+def test_denoise_errors_match_reference(gpu_ready, name):
+    rec, arr, _, pc = _input(name)
+    cls_name, msg = rec["denoise_error"].split(": ", 1)
+    with pytest.raises(getattr(fb, cls_name)) as ei:
+        fb.denoise(pc, _cfg(rec))
+    assert str(ei.value) == msg
+
+
+def test_all_excluded_fallback_warns(gpu_ready):
+    rec, arr = golden_case("checker_all_excluded")
+    pc = fb.PointCloud(arr["coords"], arr["noisy_colors"], 3)
+    with pytest.warns(UserWarning, match="excluded every point"):
+        out, rep = fb.denoise(pc, fb.FilterConfig(patch_size=3))
+    assert rep.selected_q == rec["report"]["selected_q"]
+    assert rep.masked_fraction == 0.0
+    assert np.max(np.abs(out.colors - arr["out_colors"])) <= COLOR_ATOL
+
+
+def test_denoise_is_deterministic(gpu_ready):
+    rec, arr, _, pc = _input("m20k_two-tone_s20")
+    a, ra = fb.denoise(pc)
+    b, rb = fb.denoise(pc)
+    assert np.array_equal(a.colors, b.colors)
+    assert ra.device["trace"] == rb.device["trace"]
+
+
+def test_fslr_never_changes_the_filtered_signal(gpu_ready):
+    """with a fixed q the output is identical with FSLR on or off."""
+    _, _, _, pc = _input("m20k_two-tone_s10")
+    a, _ = fb.denoise(pc, fb.FilterConfig(), cached_q=5)
+    b, _ = fb.denoise(pc, fb.FilterConfig(fslr_enabled=False), cached_q=5)
+    assert np.array_equal(a.colors, b.colors)
+
+
+def test_select_q_stage_api_matches_denoise(gpu_ready):
+    rec, arr, _, pc = _input("m20k_constant_s10")
+    g = fb.build_weighted_slg(pc)
+    est = fb.estimate_noise(pc, g)
+    ps = fb.extract_patches(pc, g, 7)
+    mask = fb.fslr_mask(ps, est.sigma_est)
+    q, x = fb.select_q(pc, g, est.sigma_est, fb.FilterConfig(), mask)
+    assert q == rec["report"]["selected_q"]
+    assert np.max(np.abs(x - arr["out_colors_f32"])) <= COLOR_ATOL
+    crit = fb.selection_criterion(pc.colors, x, mask, est.sigma_est)
+    assert crit == pytest.approx(rec["report"]["criterion_value"], rel=1e-6, abs=1e-8)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", golden_names("x1m_"))
+def test_full_size_frames(gpu_ready, name):
+    """Config 2/3 at 1M points: q, S, sigma_est, structure digests, mask, PSNR."""
+    rec, arr, clean, pc = _input(name)
+    out, rep = fb.denoise(pc, _cfg(rec), cached_q=rec.get("cached_q"),
+                          cached_sigma_est=rec.get("cached_sigma"))
+    _check_e2e(rec, arr, clean, out, rep)
+    assert rep.device["n_edges"] == rec["graph"]["n_edges"]
+    if not rec.get("cached_q"):
+        g = fb.build_slg(pc)
+        for key in ("indptr", "indices", "edge_u", "edge_v"):
+            assert digest(getattr(g, key)) == rec["graph"][f"sha_{key}"], key
+        assert rep.device["included_count"] == rec["included_count"]
+    # size-independent properties: output within the input range, sums close
+    assert out.colors.sum() == pytest.approx(rec["out_sum"], rel=1e-9)
+    assert (out.colors ** 2).sum() == pytest.approx(rec["out_sumsq"], rel=1e-9)
