@@ -182,13 +182,18 @@ def run_b200(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clk = Clocks(local).__enter__()
     for _ in range(max(args.warmup, 3)):
+        step_device()
+    # keep the GPU busy until the sampler is live so its samples cover load
+    t_wait = time.perf_counter()
+    while len(clk.lines) < 3 and time.perf_counter() - t_wait < 10.0:
         step_device()
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     reps = []
-    with Clocks(local) as clk:
+    if True:
         for k in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.fill_(k)
@@ -224,7 +229,7 @@ def run_b200(args):
     stage = {"graph_construction_ms": 1e3 * float(np.mean([r.t_graph_construction for r in reps])),
              "noise_estimation_ms": 1e3 * float(np.mean([r.t_noise_estimation for r in reps])),
              "low_pass_filter_ms": 1e3 * float(np.mean([r.t_low_pass_filter for r in reps]))}
-    clocks = clk.summary()
+    n_timed_samples = len(clk.lines)
 
     # e2e: public API, pinned host inputs, H2D + D2H inside each step
     e2e = None
@@ -259,6 +264,11 @@ def run_b200(args):
                "d2h_bytes_per_step": int(out.colors.nbytes),
                "ms_per_step": 1e3 * e2e_s / args.steps,
                "path": "paper_2401_09721_b200.denoise(PointCloud) -> fgbd_denoise C-ABI, pinned host inputs"}
+
+    clk.__exit__()
+    clocks = clk.summary()
+    clocks["window"] = "sampled every 100 ms from warm-up through the timed and e2e steps"
+    clocks["samples_before_e2e"] = n_timed_samples
 
     # CPU baseline + parity spot check (rank 0, N = 1 only)
     cpu = None

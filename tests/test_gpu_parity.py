@@ -24,6 +24,10 @@ pytestmark = pytest.mark.gpu
 COLOR_ATOL = 1e-4 * 255.0
 SIGMA_RTOL = 1e-10
 PSNR_TOL = 0.01
+# fp32 edge weights move Eq. (6) by O(1e-7) (SURVEY 8(a) a7 measured <= 2e-8 at 1M);
+# the smallest best-vs-second criterion gap in the sweeps is 4.7e-3.
+CRIT_ATOL = 1e-6
+CRIT_RTOL = 1e-6  # tiny clouds: no averaging of the per-weight rounding
 
 
 def _input(name):
@@ -174,8 +178,8 @@ def _check_e2e(rec, arr, clean, out, rep):
         assert rep.masked_fraction == r["masked_fraction"]
         assert rep.eligible_count == r["eligible_count"]
         assert rep.converged == r["converged"]
-        assert rep.criterion_value == pytest.approx(r["criterion_value"], rel=1e-6, abs=1e-8)
-        np.testing.assert_allclose(rep.device["trace"], rec["trace"], rtol=1e-6, atol=1e-8)
+        assert rep.criterion_value == pytest.approx(r["criterion_value"], rel=CRIT_RTOL, abs=CRIT_ATOL)
+        np.testing.assert_allclose(rep.device["trace"], rec["trace"], rtol=CRIT_RTOL, atol=CRIT_ATOL)
     else:
         assert rep.sigma_est == r["sigma_est"]
     if "out_colors" in arr:
@@ -244,7 +248,7 @@ def test_select_q_stage_api_matches_denoise(gpu_ready):
     assert q == rec["report"]["selected_q"]
     assert np.max(np.abs(x - arr["out_colors_f32"])) <= COLOR_ATOL
     crit = fb.selection_criterion(pc.colors, x, mask, est.sigma_est)
-    assert crit == pytest.approx(rec["report"]["criterion_value"], rel=1e-6, abs=1e-8)
+    assert crit == pytest.approx(rec["report"]["criterion_value"], rel=0, abs=CRIT_ATOL)
 
 
 @pytest.mark.slow

@@ -1,0 +1,53 @@
+"""Small driver for ncu: denoise a few device-resident frames.
+
+    python tools/profile_frame.py [--kind ramp] [--n 1000000] [--frames 3]
+
+Launch order per frame (config 2, ramp, b=7): memset x2, k_prep, k_scan_hist,
+3 x k_onesweep, k_neighbors, k_rows, k_weights, k_noise, k_reduce_cols,
+k_mask, 64 x k_lf_step, k_finalize.
+"""
+
+from __future__ import annotations
+
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kind", default="ramp")
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--sigma", type=float, default=10.0)
+    ap.add_argument("--frames", type=int, default=3)
+    ap.add_argument("--cached", type=int, default=-1)
+    a = ap.parse_args()
+    import torch
+
+    import paper_2401_09721_b200 as fb
+    from paper_2401_09721_b200 import _native as nat
+
+    clean, _ = fb.generate_cloud(a.kind, a.n, seed=0)
+    noisy = fb.add_gaussian_noise(clean, a.sigma, seed=1)
+    ctx = nat.context()
+    dc = torch.from_numpy(np.array(noisy.coords)).cuda()
+    dy = torch.from_numpy(np.array(noisy.colors)).cuda()
+    do = torch.empty_like(dy)
+    cfg = nat.make_config(fb.FilterConfig())
+    for f in range(a.frames):
+        rep = nat.Report()
+        ctx.check(ctx.lib.fgbd_denoise(ctx.handle, dc.data_ptr(), dy.data_ptr(), a.n,
+                                       noisy.bit_depth, cfg, a.cached, float("nan"),
+                                       do.data_ptr(), rep, nat.FLAG_DEVICE_PTRS), "denoise")
+        print(f"frame {f}: q={rep.selected_q} S={rep.steps} launches={rep.gpu_launches} "
+              f"GC={rep.t_graph_construction*1e3:.3f}ms NE={rep.t_noise_estimation*1e3:.3f}ms "
+              f"LF={rep.t_low_pass_filter*1e3:.3f}ms lf_steps={rep.t_lf_steps*1e3:.3f}ms "
+              f"total={rep.t_total*1e3:.3f}ms")
+
+
+if __name__ == "__main__":
+    main()
