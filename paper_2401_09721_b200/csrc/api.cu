@@ -1,6 +1,7 @@
 // C ABI (include/fgbd_b200.h): context lifetime, the `denoise` drop-in
 // (reference filtering.py:259-328) and the stage entry points.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -97,13 +98,42 @@ int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64) {
   if ((rc = dalloc(ctx, &ctx->ell, kSlots * cap))) return rc;
   if ((rc = dalloc(ctx, &ctx->meta, cap))) return rc;
   for (int k = 0; k < 3; ++k)
-    if ((rc = dalloc(ctx, &ctx->buf[k], 3 * cap))) return rc;
+    if ((rc = dalloc(ctx, &ctx->buf[k], 4 * cap))) return rc;
   if ((rc = dalloc(ctx, &ctx->out, 3 * cap))) return rc;
   if ((rc = dalloc(ctx, &ctx->fslr, cap))) return rc;
   if ((rc = dalloc(ctx, &ctx->mask, (cap + 31) / 32 + 1))) return rc;
   FGBD_CUDA(ctx, cudaMemcpy(ctx->d_bufs, ctx->buf, sizeof(ctx->buf), cudaMemcpyHostToDevice));
+  {
+    // reduction partials: one-row-per-thread kernels need 3 per block + group totals
+    const int64_t blocks = (cap + kBlock - 1) / kBlock;
+    const int64_t need = std::max<int64_t>(1 << 19, 3 * blocks + 3 * (blocks / 64 + 1) + 1024);
+    if ((rc = dalloc(ctx, &ctx->partials, need))) return rc;
+  }
   ctx->cap = cap;
   ctx->key64_cap = k64;
+  return FGBD_OK;
+}
+
+int upload_colors(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev) {
+  if (n <= 0) return FGBD_OK;
+  const double* src = colors;
+  if (!dev) {
+    FGBD_CUDA(ctx, cudaMemcpyAsync(ctx->out, colors, 3 * n * sizeof(double),
+                                   cudaMemcpyHostToDevice, ctx->stream));
+    src = ctx->out;
+  }
+  return launch_expand(ctx, src, n, BUF_Y);
+}
+
+int download_signal(fgbd_ctx* ctx, int src_buf, double* dst, int64_t n, bool dev, int clip) {
+  if (n <= 0) return FGBD_OK;
+  double* stage = dev ? dst : ctx->out;
+  int rc = launch_compact(ctx, n, src_buf, stage, clip);
+  if (rc) return rc;
+  if (!dev)
+    FGBD_CUDA(ctx, cudaMemcpyAsync(dst, ctx->out, 3 * n * sizeof(double), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+  FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return FGBD_OK;
 }
 
@@ -117,6 +147,28 @@ int ensure_w64(fgbd_ctx* ctx, int64_t n) {
 using namespace fgbd;
 
 namespace {
+
+// Optionally pin the ELL graph in L2 across the filter steps of a frame.
+void apply_l2_policy(fgbd_ctx* ctx, int64_t n) {
+  if (!ctx->l2_persist) return;
+  int max_persist = 0, max_window = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
+  const size_t bytes = (size_t)kSlots * n * sizeof(int2);
+  const size_t lim = std::min<size_t>(bytes, (size_t)max_persist);
+  const size_t win = std::min<size_t>(bytes, (size_t)max_window);
+  if (lim == 0 || win == 0) return;
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+  cudaStreamAttrValue v;
+  std::memset(&v, 0, sizeof(v));
+  v.accessPolicyWindow.base_ptr = ctx->ell;
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)lim / (float)win);
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();
+}
 
 int check_cfg(fgbd_ctx* ctx, const fgbd_config* c) {
   if (!c) return set_error(ctx, FGBD_E_ARG, "config must not be NULL");
@@ -141,6 +193,8 @@ int check_graph_input(fgbd_ctx* ctx, int64_t n, int bits) {
                                             " exceeds 21 (64-bit code overflow)");
   if (n >= (int64_t(1) << 31))
     return set_error(ctx, FGBD_E_GRAPH, "point count exceeds the 2^31 edge-encoding limit");
+  if (n > (int64_t)8192 * 64 * kBlock)
+    return set_error(ctx, FGBD_E_ARG, "frames above 134M points are not supported by this build");
   return FGBD_OK;
 }
 
@@ -266,14 +320,16 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if ((e = cudaMalloc(&ctx->ctl, sizeof(Ctl))) != cudaSuccess) return fail(e, "ctl");
   if ((e = cudaMemset(ctx->ctl, 0, sizeof(Ctl))) != cudaSuccess) return fail(e, "ctl");
   if ((e = cudaMallocHost(&ctx->ctl_host, sizeof(Ctl))) != cudaSuccess) return fail(e, "ctl host");
-  if ((e = cudaMalloc(&ctx->partials, (1 << 17) * sizeof(double))) != cudaSuccess)
-    return fail(e, "partials");
   if ((e = cudaMalloc(&ctx->sort.hist, 3 * kMaxPasses * kRadix * sizeof(uint32_t))) != cudaSuccess)
     return fail(e, "hist");
   if ((e = cudaMalloc(&ctx->sort.tile_ctr, 3 * kMaxPasses * sizeof(unsigned))) != cudaSuccess)
     return fail(e, "tile ctr");
   if ((e = cudaMalloc(&ctx->d_bufs, 3 * sizeof(double*))) != cudaSuccess) return fail(e, "bufs");
-  if (max_points > 0 && ensure_capacity(ctx, max_points, 0) != FGBD_OK) {
+  if ((e = cudaMalloc(&ctx->tickets, 8192 * sizeof(unsigned))) != cudaSuccess) return fail(e, "tickets");
+  if ((e = cudaMemset(ctx->tickets, 0, 8192 * sizeof(unsigned))) != cudaSuccess) return fail(e, "tickets");
+  if (const char* v = std::getenv("FGBD_LF_VARIANT")) ctx->lf_variant = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_L2_PERSIST")) ctx->l2_persist = std::atoi(v);
+  if (ensure_capacity(ctx, max_points > 0 ? max_points : 1, 0) != FGBD_OK) {
     set_error(nullptr, FGBD_E_CUDA, ctx->err);
     fgbd_ctx_destroy(ctx);
     return nullptr;
@@ -292,6 +348,7 @@ void fgbd_ctx_destroy(fgbd_ctx* ctx) {
   if (ctx->sort.hist) cudaFree(ctx->sort.hist);
   if (ctx->sort.tile_ctr) cudaFree(ctx->sort.tile_ctr);
   if (ctx->d_bufs) cudaFree(ctx->d_bufs);
+  if (ctx->tickets) cudaFree(ctx->tickets);
   if (ctx->csr_scratch) cudaFree(ctx->csr_scratch);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
@@ -344,7 +401,8 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   cudaEvent_t* ev = ctx->ev;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   if ((rc = ensure_capacity(ctx, n, 3 * bits > 32))) return rc;
-  if ((rc = h2d(ctx, ctx->buf[BUF_Y], colors, 3 * n * sizeof(double), dev))) return rc;
+  apply_l2_policy(ctx, n);
+  if ((rc = upload_colors(ctx, colors, n, dev))) return rc;
   if (!dev && (rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false))) return rc;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
   if ((rc = stage_graph(ctx, dev ? coords : ctx->coords64, n, bits, true, w64))) return rc;
@@ -357,7 +415,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     int fin = BUF_Y;
     if ((rc = launch_fixed_steps(ctx, n, cached_q, w64, &fin))) return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
-    if ((rc = launch_finalize(ctx, n, fin, ctx->out))) return rc;
+    if ((rc = launch_compact(ctx, n, fin, dev ? out_colors : ctx->out, 1))) return rc;
   } else {
     const int D = cfg->patch_size;
     if ((rc = launch_noise(ctx, n, D))) return rc;
@@ -371,17 +429,16 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = finish_noise(ctx, D, cfg->tau_divisor, &nz))) return rc;
     const double sig = nz.sigma_est;
     const int active = cfg->fslr_enabled && !(sig < cfg->fslr_sigma_floor);
-    if ((rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode, nullptr)))
+    if ((rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode, cfg->early_exit,
+                          nullptr)))
       return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
-    if ((rc = launch_select_steps(ctx, n, cfg->q_max, cfg->criterion_mode, cfg->early_exit, sig,
-                                  w64)))
-      return rc;
+    if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
-    if ((rc = launch_finalize(ctx, n, -1, ctx->out))) return rc;
+    if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   }
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
-  if ((rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), dev))) return rc;
+  if (!dev && (rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), false))) return rc;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
   if ((rc = pull_ctl(ctx))) return rc;
   if ((rc = check_graph_ctl(ctx, bits))) return rc;
@@ -595,7 +652,7 @@ int32_t fgbd_estimate_noise(fgbd_ctx* ctx, const double* colors, int32_t patch_s
                                             " exceeds 1 + max degree (" + std::to_string(1 + maxdeg) +
                                             ") of this graph");
   const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
-  int rc = h2d(ctx, ctx->buf[BUF_Y], colors, 3 * n * sizeof(double), dev);
+  int rc = upload_colors(ctx, colors, n, dev);
   if (rc) return rc;
   if ((rc = launch_noise(ctx, n, D))) return rc;
   if ((rc = pull_ctl(ctx))) return rc;
@@ -619,7 +676,7 @@ int32_t fgbd_fslr_mask(fgbd_ctx* ctx, double sigma_est, double sigma_floor, uint
     return set_error(ctx, FGBD_E_NOISE, "run fgbd_estimate_noise before fgbd_fslr_mask");
   const int64_t n = ctx->g_n;
   const int active = !(sigma_est < sigma_floor);
-  int rc = launch_mask(ctx, n, sigma_est, active, 0, FGBD_CRIT_POOLED, nullptr);
+  int rc = launch_mask(ctx, n, sigma_est, active, 0, FGBD_CRIT_POOLED, 0, nullptr);
   if (rc) return rc;
   std::vector<uint32_t> bits((n + 31) / 32);
   FGBD_CUDA(ctx, cudaMemcpyAsync(bits.data(), ctx->mask, bits.size() * 4, cudaMemcpyDeviceToHost,
@@ -690,13 +747,11 @@ int32_t fgbd_apply_filter(fgbd_ctx* ctx, const double* colors_in, int32_t q, dou
     if (n) FGBD_CUDA(ctx, cudaMemcpy(colors_out, colors_in, 3 * n * 8, cudaMemcpyDefault));
     return FGBD_OK;
   }
-  int rc = h2d(ctx, ctx->buf[BUF_Y], colors_in, 3 * n * 8, dev);
+  int rc = upload_colors(ctx, colors_in, n, dev);
   if (rc) return rc;
   int fin = BUF_Y;
   if ((rc = launch_fixed_steps(ctx, n, q, ctx->g_weights64, &fin))) return rc;
-  if ((rc = d2h(ctx, colors_out, ctx->buf[fin], 3 * n * 8, dev))) return rc;
-  FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  return FGBD_OK;
+  return download_signal(ctx, fin, colors_out, n, dev, 0);
 }
 
 int32_t fgbd_select_q(fgbd_ctx* ctx, const double* colors, const uint8_t* include,
@@ -715,7 +770,7 @@ int32_t fgbd_select_q(fgbd_ctx* ctx, const double* colors, const uint8_t* includ
   if (ctx->g_n < 0) return set_error(ctx, FGBD_E_GRAPH, "no graph held by this context");
   const int64_t n = ctx->g_n;
   const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
-  if ((rc = h2d(ctx, ctx->buf[BUF_Y], colors, 3 * n * 8, dev))) return rc;
+  if ((rc = upload_colors(ctx, colors, n, dev))) return rc;
   uint8_t* d_inc = nullptr;
   std::vector<uint8_t> ones;
   if (include) {
@@ -730,10 +785,8 @@ int32_t fgbd_select_q(fgbd_ctx* ctx, const double* colors, const uint8_t* includ
     FGBD_CUDA(ctx, cudaMalloc(&d_inc, n));
     FGBD_CUDA(ctx, cudaMemcpy(d_inc, ones.data(), n, cudaMemcpyHostToDevice));
   }
-  rc = launch_mask(ctx, n, sigma_est, 0, cfg->q_max, cfg->criterion_mode, d_inc);
-  if (rc == FGBD_OK)
-    rc = launch_select_steps(ctx, n, cfg->q_max, cfg->criterion_mode, cfg->early_exit, sigma_est,
-                             ctx->g_weights64);
+  rc = launch_mask(ctx, n, sigma_est, 0, cfg->q_max, cfg->criterion_mode, cfg->early_exit, d_inc);
+  if (rc == FGBD_OK) rc = launch_select_steps(ctx, n, cfg->q_max, ctx->g_weights64);
   if (rc == FGBD_OK) rc = pull_ctl(ctx);
   cudaFree(d_inc);
   if (rc) return rc;
@@ -741,10 +794,7 @@ int32_t fgbd_select_q(fgbd_ctx* ctx, const double* colors, const uint8_t* includ
   if (h.included < 1)
     return set_error(ctx, FGBD_E_FILTER, "criterion needs at least one included point");
   if (q_out) *q_out = h.best_q;
-  if (x_out) {
-    if ((rc = d2h(ctx, x_out, ctx->buf[h.best_buf], 3 * n * 8, dev))) return rc;
-    FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  }
+  if (x_out && (rc = download_signal(ctx, h.best_buf, x_out, n, dev, 0))) return rc;
   if (rep) {
     std::memset(rep, 0, sizeof(*rep));
     rep->selected_q = h.best_q;

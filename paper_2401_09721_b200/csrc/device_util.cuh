@@ -65,6 +65,66 @@ __device__ __forceinline__ bool last_block(unsigned int* ticket, bool* s_flag) {
   return *s_flag;
 }
 
+// Like last_block, for a counter shared by `count` blocks.
+__device__ __forceinline__ bool last_block_of(unsigned int* ticket, int count, bool* s_flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned t = atomicAdd(ticket, 1u);
+    *s_flag = (t == (unsigned)count - 1);
+  }
+  __syncthreads();
+  if (*s_flag) __threadfence();
+  return *s_flag;
+}
+
+// 256-bit signal row access (LDG/STG.E.ENL2.256 on sm_100a).  The compiler
+// splits a double4 load whose 4th lane is unused into 128 + 64 bits, which
+// doubles the L1 wavefronts of a gather; inline PTX keeps it one sector.
+__device__ __forceinline__ double4 ld_row(const double4* p) {
+  double4 v;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_row(double4* p, double4 v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z),
+               "d"(v.w)
+               : "memory");
+}
+
+// L2 eviction-priority policies (createpolicy, sm_80+) and hinted accesses.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double4 ld_row_hint(const double4* p, uint64_t pol) {
+  double4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_row_hint(double4* p, double4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v.x),
+               "d"(v.y), "d"(v.z), "d"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ int2 ld_slot_hint(const int2* p, uint64_t pol) {
+  int2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
 }  // namespace fgbd

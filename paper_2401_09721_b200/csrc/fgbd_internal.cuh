@@ -11,7 +11,8 @@
 //             until the weight pass replaces it by the fp32 Gaussian weight;
 //             padding slots hold (self, 0)
 //   meta      per point: degree (3 bits) | patch order (6 x 3 bits)
-//   buf[3]    fp64 (N,3) signals: Y = noisy input, A, B (select_q rotation)
+//   buf[3]    fp64 (N,4) signals (r,g,b,0) -- one 32 B sector per point:
+//             Y = noisy input, A, B (select_q rotation)
 //   fslr      per point FSLR statistic (fp64, -1 = not eligible)
 //   mask      1 bit per point (FSLR include)
 //   ctl       device control block (reductions, select_q state)
@@ -28,14 +29,13 @@ namespace fgbd {
 
 constexpr int kBlock = 256;
 constexpr int kRedGrid = 148 * 4;      // fixed partition => deterministic sums
-constexpr int kNeGrid = 148 * 6;       // NE blocks (96 threads: one warp per channel)
+constexpr int kNeGrid = 148 * 16;      // NE blocks (96 threads: one warp per channel)
 constexpr int kSortThreads = 256;
 constexpr int kSortIPT = 16;
 constexpr int kSortTile = kSortThreads * kSortIPT;  // keys per onesweep tile
 constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;
 constexpr int kSlots = 6;              // max SLG degree: 2 neighbours x 3 lines
-constexpr int kMom = 35;               // 7 first + 28 second moments per channel
 
 enum BufId { BUF_Y = 0, BUF_A = 1, BUF_B = 2 };
 
@@ -49,7 +49,7 @@ struct Ctl {
   int err_flags;  // bit0: coordinate out of range
   // noise estimation
   long long eligible;
-  double mom[3][kMom];
+  double gram[3][64];  // per-channel 8x8 Gram matrix of shifted patch rows
   // FSLR mask
   long long included;
   int mask_all;
@@ -66,6 +66,10 @@ struct Ctl {
   int best_buf;
   double best_crit;
   double prev_crit;
+  double sv2;       // sigma_est^2
+  int q_max;
+  int mode;         // FGBD_CRIT_*
+  int early_exit;
   double trace[FGBD_TRACE_MAX];
   unsigned int ticket[8];
 };
@@ -100,11 +104,15 @@ struct fgbd_ctx {
   int2* ell = nullptr;          // [6][N]
   double* w64 = nullptr;        // [6][N] fp64 weights (parity mode, lazy)
   uint32_t* meta = nullptr;     // [N]
-  double* buf[3] = {};          // Y, A, B signals (N,3) fp64
+  double* buf[3] = {};          // Y, A, B signals (N,4) fp64
   double* out = nullptr;        // (N,3) fp64 result staging
   double* fslr = nullptr;       // [N]
   uint32_t* mask = nullptr;     // [ceil(N/32)]
-  double* partials = nullptr;   // reduction partials
+  double* partials = nullptr;   // reduction partials (1<<17 doubles)
+  unsigned int* tickets = nullptr;  // group tickets for hierarchical reductions
+  int lf_variant = 5;           // filter-step kernel (FGBD_LF_VARIANT): 0 per-step, 2+ persistent
+  int coop_blocks[64] = {};      // co-resident grid of each persistent instantiation
+  int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   fgbd::Ctl* ctl = nullptr;     // device
   fgbd::Ctl* ctl_host = nullptr;  // pinned mirror
   // scratch for CSR export / injection (lazy)
@@ -145,6 +153,10 @@ int cuda_error(fgbd_ctx* ctx, cudaError_t e, const char* where);
   } while (0)
 
 int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64);
+// (N,3) colours (host or device) -> BUF_Y in the (N,4) layout
+int upload_colors(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev);
+// signal buffer (src_buf < 0: the select_q best) -> (N,3) host/device array
+int download_signal(fgbd_ctx* ctx, int src_buf, double* dst, int64_t n, bool dev, int clip);
 int ensure_w64(fgbd_ctx* ctx, int64_t n);
 
 // ---- graph construction (graph.cu) --------------------------------------
@@ -178,12 +190,14 @@ int select_tail_host(const double* lam, int d, int divisor, int* m, double* tau,
                      int* fallback, std::string* err);
 
 // ---- filter (filter.cu) --------------------------------------------------
-int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active,
-                int q_max, int mode, const uint8_t* d_include_bytes);
-int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int mode, int early_exit,
-                        double sigma_est, int w64);
+// (N,3) device colours -> signal buffer `buf` in the (N,4) layout
+int launch_expand(fgbd_ctx* ctx, const double* d_src, int64_t n, int buf);
+// signal buffer (or the select_q best buffer when src_buf < 0) -> (N,3), optional clip
+int launch_compact(fgbd_ctx* ctx, int64_t n, int src_buf, double* d_dst, int clip);
+int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_max, int mode,
+                int early_exit, const uint8_t* d_include_bytes);
+int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64);
 int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf);
-int launch_finalize(fgbd_ctx* ctx, int64_t n, int src_buf_or_neg, double* d_out);
 int launch_csr_steps(fgbd_ctx* ctx, const int64_t* d_indptr, const int64_t* d_indices,
                      const double* d_w, int64_t n, const double* d_in, double* d_tmp,
                      double* d_out, int q);

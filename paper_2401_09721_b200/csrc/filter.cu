@@ -1,24 +1,35 @@
 // FSLR mask, random-walk low-pass filter and the device-resident q scan
 // (reference filtering.py:132-256).
 //
-// k_mask        include_i = !(eligible_i && stat_i > 2 sigma_est), packed to
-//               1 bit/point with a warp ballot; sums count and sum_inc y^2;
-//               its last block initialises the select_q state (q = 0).
-// k_lf_step     one filter step out = (d f + sum_j w_ij f_j) / (2 d) over the
-//               ELL graph, exactly the reference's arithmetic order (slot
-//               order accumulation from 0.0, no FMA; d = sum_{j>i} w +
-//               sum_{j<i} w), fused with the masked sum of out^2.  Its last
-//               block evaluates Eq. (6) and runs select_q's bookkeeping
-//               (strict improvement, 3-rise early exit, best_crit == 0 stop)
-//               and rotates the three signal buffers, so the q loop needs no
-//               host round trip: later launches see `stop` and return.
-// k_finalize    clip(best, 0, 255) (filtering.py:327).
+// Signals live in HBM as (N, 4) fp64 rows (r, g, b, 0): one 32-byte sector
+// per point, so every neighbour gather is a single 256-bit load
+// (LDG.E.ENL2.256 on sm_100a) instead of three 8-byte loads.
+//
+// k_mask       include_i = !(eligible_i && stat_i > 2 sigma_est), packed to
+//              1 bit/point by warp ballot; sums count and sum_inc y^2; its
+//              last block initialises the select_q state (q = 0).
+// k_lf_persist the whole q scan in ONE cooperative launch: every block owns
+//              a fixed set of rows; per step it applies
+//              out = (d f + sum_j w_ij f_j) / (2 d) in the reference's exact
+//              arithmetic order (slot-order accumulation from 0.0, no FMA,
+//              d = sum_{j>i} w + sum_{j<i} w), adds its rows' masked out^2 to
+//              a block partial, and after grid.sync() every block reduces
+//              the partials in the same fixed order, evaluates Eq. (6) and
+//              runs select_q's bookkeeping (strict improvement, 3-rise early
+//              exit, best_crit == 0 stop) identically -- no host round trip,
+//              no launch per step, no empty launches after early exit.
+// k_lf_step    one step per launch (variant 0, kept for comparison).
+// k_compact    (N,4) -> (N,3), optionally clipped to [0, 255] (filtering.py:327).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 #include <vector>
 
 #include "device_util.cuh"
 #include "fgbd_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace fgbd {
 
@@ -36,9 +47,44 @@ __device__ __forceinline__ double criterion(const double sy[3], const double sx[
   return acc / 3.0;
 }
 
+// ---------------------------------------------------------------------------
+// layout conversion
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kBlock) k_expand(const double* __restrict__ src, int64_t n,
+                                                   double4* __restrict__ dst) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    st_row(dst + i, make_double4(src[3 * i], src[3 * i + 1], src[3 * i + 2], 0.0));
+}
+
+template <bool CLIP>
+__global__ void __launch_bounds__(kBlock) k_compact(double* const* bufs, const Ctl* ctl,
+                                                    const double4* src, int64_t n,
+                                                    double* __restrict__ dst) {
+  const double4* s = src ? src : reinterpret_cast<const double4*>(bufs[ctl->best_buf]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double4 v = ld_row(s + i);
+    if (CLIP) {
+      dst[3 * i] = fmin(fmax(v.x, 0.0), 255.0);
+      dst[3 * i + 1] = fmin(fmax(v.y, 0.0), 255.0);
+      dst[3 * i + 2] = fmin(fmax(v.z, 0.0), 255.0);
+    } else {
+      dst[3 * i] = v.x;
+      dst[3 * i + 1] = v.y;
+      dst[3 * i + 2] = v.z;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FSLR mask + select_q initialisation
+// ---------------------------------------------------------------------------
+
 struct MaskArgs {
   const double* fslr;
-  const double* y;
+  const double4* y;
   const uint8_t* inc_bytes;  // explicit mask (stage API) or null
   int64_t n;
   double thr;
@@ -48,6 +94,7 @@ struct MaskArgs {
   Ctl* ctl;
   int q_max;
   int mode;
+  int early_exit;
   double sv2;
 };
 
@@ -68,12 +115,12 @@ __global__ void __launch_bounds__(kBlock) k_mask(MaskArgs a) {
     const unsigned bits = __ballot_sync(kFull, inc);
     if (lane == 0 && i < a.n) a.mask[i >> 5] = bits;
     if (valid) {
+      const double4 y = ld_row(a.y + i);
+      const double y2[3] = {y.x * y.x, y.y * y.y, y.z * y.z};
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double y = a.y[3 * i + c];
-        const double y2 = y * y;
-        v[4 + c] += y2;
-        if (inc) v[1 + c] += y2;
+        v[4 + c] += y2[c];
+        if (inc) v[1 + c] += y2[c];
       }
       v[0] += inc ? 1.0 : 0.0;
     }
@@ -113,34 +160,302 @@ __global__ void __launch_bounds__(kBlock) k_mask(MaskArgs a) {
       c->out_buf = BUF_A;
       c->stop = (a.q_max <= 0) || (crit0 == 0.0) || (cnt < 1);
       c->trace[0] = crit0;
+      c->sv2 = a.sv2;
+      c->q_max = a.q_max;
+      c->mode = a.mode;
+      c->early_exit = a.early_exit;
       c->ticket[1] = 0;
     }
   }
 }
 
+// ---------------------------------------------------------------------------
+// the filter step
+// ---------------------------------------------------------------------------
+
 struct StepArgs {
   const int2* ell;
   const double* w64;
-  double* buf[3];
-  const double* in;  // fixed mode
-  double* out;       // fixed mode
+  double4* buf[3];
   const uint32_t* mask;
   int64_t n;
-  double* part;  // [3][grid]
+  double* part;  // [2 parities][3][grid]
   Ctl* ctl;
-  int q_max;
-  int mode;
-  int early_exit;
-  double sv2;
+  int fixed_steps;  // > 0: cached path, no criterion (Y -> A/B ping-pong)
 };
 
+// One random-walk step for row i (filtering.py:132-155), reference order.
+template <bool W64>
+__device__ __forceinline__ double4 lf_row(const int2* __restrict__ ell,
+                                          const double* __restrict__ w64,
+                                          const double4* in, int64_t n, int64_t i) {
+  int nb[kSlots];
+  double w[kSlots];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    const int2 sl = __ldg(&ell[s * n + i]);
+    nb[s] = sl.x;
+    w[s] = W64 ? __ldg(&w64[s * n + i]) : (double)__int_as_float(sl.y);
+  }
+  const double4 f = ld_row(in + i);
+  double4 g[kSlots];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) g[s] = (w[s] != 0.0) ? ld_row(in + nb[s]) : make_double4(0, 0, 0, 0);
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    if (nb[s] < (int)i) lo = __dadd_rn(lo, w[s]);
+    else if (nb[s] > (int)i) hi = __dadd_rn(hi, w[s]);
+    if (w[s] != 0.0) {
+      acc0 = __dadd_rn(acc0, __dmul_rn(w[s], g[s].x));
+      acc1 = __dadd_rn(acc1, __dmul_rn(w[s], g[s].y));
+      acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g[s].z));
+    }
+  }
+  const double d = __dadd_rn(hi, lo);
+  if (d == 0.0) return f;
+  const double d2 = __dmul_rn(2.0, d);
+  return make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
+                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
+                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
+}
+
+// Same arithmetic as lf_row; ELL streamed with evict_first, signal rows
+// kept with evict_last so x_out of step q is still in L2 for step q+1.
+__device__ __forceinline__ double4 lf_row_hint(const int2* __restrict__ ell, const double4* in,
+                                               int64_t n, int64_t i, uint64_t pol_stream,
+                                               uint64_t pol_keep) {
+  int nb[kSlots];
+  double w[kSlots];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    const int2 sl = ld_slot_hint(ell + s * n + i, pol_stream);
+    nb[s] = sl.x;
+    w[s] = (double)__int_as_float(sl.y);
+  }
+  const double4 f = ld_row_hint(in + i, pol_keep);
+  double4 g[kSlots];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s)
+    g[s] = (w[s] != 0.0) ? ld_row_hint(in + nb[s], pol_keep) : make_double4(0, 0, 0, 0);
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    if (nb[s] < (int)i) lo = __dadd_rn(lo, w[s]);
+    else if (nb[s] > (int)i) hi = __dadd_rn(hi, w[s]);
+    if (w[s] != 0.0) {
+      acc0 = __dadd_rn(acc0, __dmul_rn(w[s], g[s].x));
+      acc1 = __dadd_rn(acc1, __dmul_rn(w[s], g[s].y));
+      acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g[s].z));
+    }
+  }
+  const double d = __dadd_rn(hi, lo);
+  if (d == 0.0) return f;
+  const double d2 = __dmul_rn(2.0, d);
+  return make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
+                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
+                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
+}
+
+// select_q bookkeeping after step q (filtering.py:244-255).  Pure function
+// of (state, crit): every block evaluates it identically.
+struct SelState {
+  int q, best_q, streak, stop, in_b, out_b, best_b;
+  double best_crit, prev;
+};
+
+__device__ __forceinline__ void select_update(SelState& s, double crit, int q_max,
+                                              int early_exit) {
+  s.q += 1;
+  if (crit < s.best_crit) {
+    s.best_crit = crit;
+    s.best_q = s.q;
+    s.best_b = s.out_b;
+  }
+  s.streak = crit > s.prev ? s.streak + 1 : 0;
+  s.prev = crit;
+  s.stop = (early_exit && s.streak >= 3) || (s.q >= q_max) || (s.best_crit == 0.0);
+  const int nin = s.out_b;
+  int nout = BUF_A;  // first of A, B, Y that is neither the new input nor the best
+  if (nout == nin || nout == s.best_b) nout = BUF_B;
+  if (nout == nin || nout == s.best_b) nout = BUF_Y;
+  s.in_b = nin;
+  s.out_b = nout;
+}
+
+// Row kernel with the next row's ELL slots prefetched while the current
+// row's neighbour gathers are in flight (software pipelining).
+template <bool W64>
+__device__ __forceinline__ void load_slots(const int2* __restrict__ ell,
+                                           const double* __restrict__ w64, int64_t n,
+                                           int64_t i, int (&nb)[kSlots], double (&w)[kSlots]) {
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    const int2 sl = __ldg(&ell[s * n + i]);
+    nb[s] = sl.x;
+    w[s] = W64 ? __ldg(&w64[s * n + i]) : (double)__int_as_float(sl.y);
+  }
+}
+
+template <bool W64>
+__device__ __forceinline__ double4 lf_row_pre(const int (&nb)[kSlots], const double (&w)[kSlots],
+                                              const double4* in, int64_t i) {
+  const double4 f = ld_row(in + i);
+  double4 g[kSlots];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) g[s] = (w[s] != 0.0) ? ld_row(in + nb[s]) : make_double4(0, 0, 0, 0);
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    if (nb[s] < (int)i) lo = __dadd_rn(lo, w[s]);
+    else if (nb[s] > (int)i) hi = __dadd_rn(hi, w[s]);
+    if (w[s] != 0.0) {
+      acc0 = __dadd_rn(acc0, __dmul_rn(w[s], g[s].x));
+      acc1 = __dadd_rn(acc1, __dmul_rn(w[s], g[s].y));
+      acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g[s].z));
+    }
+  }
+  const double d = __dadd_rn(hi, lo);
+  if (d == 0.0) return f;
+  const double d2 = __dmul_rn(2.0, d);
+  return make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
+                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
+                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
+}
+
+template <bool W64, bool SELECT, bool PIPE, int MINB, bool HINT = false>
+__global__ void __launch_bounds__(kBlock, MINB) k_lf_persist(StepArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double s_red[32 * 3];
+  // select_q state is block-uniform: thread 0 owns it, the block reads it
+  __shared__ SelState s_st;
+  __shared__ double s_sy[3], s_sv2;
+  __shared__ long long s_inc;
+  __shared__ int s_qmax, s_mode, s_early, s_mask_all;
+  Ctl* ctl = a.ctl;
+  const int64_t n = a.n;
+  const int nb = gridDim.x;
+  if (threadIdx.x == 0) {
+    if (SELECT) {
+      s_st = SelState{ctl->q, ctl->best_q, ctl->streak, ctl->stop, ctl->in_buf, ctl->out_buf,
+                      ctl->best_buf, ctl->best_crit, ctl->prev_crit};
+      for (int k = 0; k < 3; ++k) s_sy[k] = ctl->sy[k];
+      s_sv2 = ctl->sv2;
+      s_inc = ctl->included;
+      s_qmax = ctl->q_max;
+      s_mode = ctl->mode;
+      s_early = ctl->early_exit;
+      s_mask_all = ctl->mask_all;
+    } else {
+      s_st = SelState{0, 0, 0, a.fixed_steps <= 0, BUF_Y, BUF_A, BUF_Y, 0.0, 0.0};
+      s_qmax = a.fixed_steps;
+      s_mask_all = 1;
+    }
+  }
+  __syncthreads();
+  const bool mask_all = s_mask_all != 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  while (!s_st.stop) {
+    const int ib = s_st.in_b, ob = s_st.out_b, q = s_st.q;
+    const double4* in = ib == 0 ? a.buf[0] : (ib == 1 ? a.buf[1] : a.buf[2]);
+    double4* out = ob == 0 ? a.buf[0] : (ob == 1 ? a.buf[1] : a.buf[2]);
+    double sx[3] = {0.0, 0.0, 0.0};
+    if (HINT && !W64) {
+      const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double4 o = lf_row_hint(a.ell, in, n, i, pol_stream, pol_keep);
+        st_row_hint(out + i, o, pol_keep);
+        if (SELECT && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+          sx[0] = fma(o.x, o.x, sx[0]);
+          sx[1] = fma(o.y, o.y, sx[1]);
+          sx[2] = fma(o.z, o.z, sx[2]);
+        }
+      }
+    } else if (PIPE) {
+      int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+      int nbr[kSlots], nbn[kSlots];
+      double w[kSlots], wn[kSlots];
+      if (i < n) load_slots<W64>(a.ell, a.w64, n, i, nbn, wn);
+      while (i < n) {
+#pragma unroll
+        for (int s = 0; s < kSlots; ++s) {
+          nbr[s] = nbn[s];
+          w[s] = wn[s];
+        }
+        const int64_t inext = i + stride;
+        if (inext < n) load_slots<W64>(a.ell, a.w64, n, inext, nbn, wn);
+        const double4 o = lf_row_pre<W64>(nbr, w, in, i);
+        st_row(out + i, o);
+        if (SELECT && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+          sx[0] = fma(o.x, o.x, sx[0]);
+          sx[1] = fma(o.y, o.y, sx[1]);
+          sx[2] = fma(o.z, o.z, sx[2]);
+        }
+        i = inext;
+      }
+    } else {
+      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double4 o = lf_row<W64>(a.ell, a.w64, in, n, i);
+        st_row(out + i, o);
+        if (SELECT && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+          sx[0] = fma(o.x, o.x, sx[0]);
+          sx[1] = fma(o.y, o.y, sx[1]);
+          sx[2] = fma(o.z, o.z, sx[2]);
+        }
+      }
+    }
+    double* part = a.part + (q & 1) * 3 * nb;
+    if (SELECT) {
+      block_sum<3>(sx, s_red);
+      if (threadIdx.x == 0)
+        for (int k = 0; k < 3; ++k) part[k * nb + blockIdx.x] = sx[k];
+    }
+    grid.sync();
+    if (SELECT) {
+      // every block reduces the same partials in the same order -> the
+      // same criterion bits and the same decision everywhere
+      double t[3] = {0.0, 0.0, 0.0};
+      for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t[k] += __ldcg(&part[k * nb + b]);
+      block_sum<3>(t, s_red);  // ends with __syncthreads
+      if (threadIdx.x == 0) {
+        const double crit = criterion(s_sy, t, s_inc, s_sv2, s_mode);
+        select_update(s_st, crit, s_qmax, s_early);
+        if (blockIdx.x == 0 && s_st.q < FGBD_TRACE_MAX) ctl->trace[s_st.q] = crit;
+      }
+    } else if (threadIdx.x == 0) {
+      s_st.q += 1;
+      s_st.stop = s_st.q >= s_qmax;
+      const int nin = s_st.out_b;
+      s_st.out_b = (nin == BUF_A) ? BUF_B : BUF_A;
+      s_st.in_b = nin;
+      s_st.best_b = nin;
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->q = s_st.q;
+    ctl->steps = s_st.q;
+    ctl->best_q = s_st.best_q;
+    ctl->best_crit = s_st.best_crit;
+    ctl->best_buf = s_st.best_b;
+    ctl->in_buf = s_st.in_b;
+    ctl->out_buf = s_st.out_b;
+    ctl->streak = s_st.streak;
+    ctl->prev_crit = s_st.prev;
+    ctl->stop = 1;
+  }
+}
+
+// Variant 0: one step per launch (grid-stride rows, last-block decision).
 template <bool W64, bool SELECT>
-__global__ void __launch_bounds__(kBlock) k_lf_step(StepArgs a) {
+__global__ void __launch_bounds__(kBlock) k_lf_step(StepArgs a, int fin, int fout) {
   __shared__ double s_red[32 * 3];
   __shared__ bool s_last;
   Ctl* ctl = a.ctl;
-  const double* __restrict__ in;
-  double* __restrict__ out;
+  const double4* in;
+  double4* out;
   bool mask_all = true;
   if (SELECT) {
     if (*(volatile int*)&ctl->stop) return;
@@ -148,63 +463,19 @@ __global__ void __launch_bounds__(kBlock) k_lf_step(StepArgs a) {
     out = a.buf[ctl->out_buf];
     mask_all = ctl->mask_all != 0;
   } else {
-    in = a.in;
-    out = a.out;
+    in = a.buf[fin];
+    out = a.buf[fout];
   }
   const int64_t n = a.n;
   double sx[3] = {0.0, 0.0, 0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    int nb[kSlots];
-    double w[kSlots];
-#pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
-      const int2 sl = __ldg(&a.ell[s * n + i]);
-      nb[s] = sl.x;
-      w[s] = W64 ? __ldg(&a.w64[s * n + i]) : (double)__int_as_float(sl.y);
-    }
-    const double f0 = in[3 * i], f1 = in[3 * i + 1], f2 = in[3 * i + 2];
-    double g[kSlots][3];
-#pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
-      if (w[s] != 0.0) {
-        const double* p = in + 3 * (int64_t)nb[s];
-        g[s][0] = p[0];
-        g[s][1] = p[1];
-        g[s][2] = p[2];
-      } else {
-        g[s][0] = g[s][1] = g[s][2] = 0.0;
-      }
-    }
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
-#pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
-      if (nb[s] < (int)i) lo = __dadd_rn(lo, w[s]);
-      else if (nb[s] > (int)i) hi = __dadd_rn(hi, w[s]);
-      if (w[s] != 0.0) {
-        acc0 = __dadd_rn(acc0, __dmul_rn(w[s], g[s][0]));
-        acc1 = __dadd_rn(acc1, __dmul_rn(w[s], g[s][1]));
-        acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g[s][2]));
-      }
-    }
-    const double d = __dadd_rn(hi, lo);
-    double o0 = f0, o1 = f1, o2 = f2;
-    if (d != 0.0) {
-      const double d2 = __dmul_rn(2.0, d);
-      o0 = __ddiv_rn(__dadd_rn(__dmul_rn(d, f0), acc0), d2);
-      o1 = __ddiv_rn(__dadd_rn(__dmul_rn(d, f1), acc1), d2);
-      o2 = __ddiv_rn(__dadd_rn(__dmul_rn(d, f2), acc2), d2);
-    }
-    out[3 * i] = o0;
-    out[3 * i + 1] = o1;
-    out[3 * i + 2] = o2;
-    if (SELECT) {
-      const bool inc = mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u);
-      if (inc) {
-        sx[0] = fma(o0, o0, sx[0]);
-        sx[1] = fma(o1, o1, sx[1]);
-        sx[2] = fma(o2, o2, sx[2]);
-      }
+    const double4 o = lf_row<W64>(a.ell, a.w64, in, n, i);
+    st_row(out + i, o);
+    if (SELECT && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+      sx[0] = fma(o.x, o.x, sx[0]);
+      sx[1] = fma(o.y, o.y, sx[1]);
+      sx[2] = fma(o.z, o.z, sx[2]);
     }
   }
   if (!SELECT) return;
@@ -218,42 +489,24 @@ __global__ void __launch_bounds__(kBlock) k_lf_step(StepArgs a) {
       for (int k = 0; k < 3; ++k) t[k] += ld_cg(&a.part[k * gridDim.x + b]);
     block_sum<3>(t, s_red);
     if (threadIdx.x == 0) {
-      const double crit = criterion(ctl->sy, t, ctl->included, a.sv2, a.mode);
-      const int q = ctl->q + 1;
-      ctl->q = q;
-      ctl->steps = q;
-      if (q < FGBD_TRACE_MAX) ctl->trace[q] = crit;
-      if (crit < ctl->best_crit) {
-        ctl->best_crit = crit;
-        ctl->best_q = q;
-        ctl->best_buf = ctl->out_buf;
-      }
-      ctl->streak = crit > ctl->prev_crit ? ctl->streak + 1 : 0;
-      ctl->prev_crit = crit;
-      ctl->stop = (a.early_exit && ctl->streak >= 3) || (q >= a.q_max) ||
-                  (ctl->best_crit == 0.0);
-      const int nin = ctl->out_buf;
-      int nout = BUF_A;
-      const int order[3] = {BUF_A, BUF_B, BUF_Y};
-      for (int k = 0; k < 3; ++k)
-        if (order[k] != nin && order[k] != ctl->best_buf) {
-          nout = order[k];
-          break;
-        }
-      ctl->in_buf = nin;
-      ctl->out_buf = nout;
+      SelState st{ctl->q, ctl->best_q, ctl->streak, ctl->stop, ctl->in_buf, ctl->out_buf,
+                  ctl->best_buf, ctl->best_crit, ctl->prev_crit};
+      const double crit = criterion(ctl->sy, t, ctl->included, ctl->sv2, ctl->mode);
+      select_update(st, crit, ctl->q_max, ctl->early_exit);
+      if (st.q < FGBD_TRACE_MAX) ctl->trace[st.q] = crit;
+      ctl->q = st.q;
+      ctl->steps = st.q;
+      ctl->best_q = st.best_q;
+      ctl->best_crit = st.best_crit;
+      ctl->best_buf = st.best_b;
+      ctl->in_buf = st.in_b;
+      ctl->out_buf = st.out_b;
+      ctl->streak = st.streak;
+      ctl->prev_crit = st.prev;
+      ctl->stop = st.stop;
       ctl->ticket[2] = 0;
     }
   }
-}
-
-__global__ void __launch_bounds__(kBlock) k_finalize(const double* const* bufs, const Ctl* ctl,
-                                                     const double* src, int64_t n3,
-                                                     double* __restrict__ dst) {
-  const double* s = src ? src : bufs[ctl->best_buf];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n3; k += stride)
-    dst[k] = fmin(fmax(s[k], 0.0), 255.0);
 }
 
 // CSR step with caller-supplied fp64 slot weights (weight-injection parity).
@@ -283,7 +536,7 @@ __global__ void __launch_bounds__(kBlock) k_lf_csr(const int64_t* __restrict__ i
   }
 }
 
-// masked sums for selection_criterion: part[8][grid] = count, sy[3], sx[3]
+// masked sums for selection_criterion: part[7][grid] = count, sy[3], sx[3]
 __global__ void __launch_bounds__(kBlock) k_crit_sums(const double* __restrict__ y,
                                                       const double* __restrict__ x,
                                                       const uint8_t* __restrict__ inc,
@@ -314,11 +567,33 @@ static int red_grid(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, kRedGrid));
 }
 
+static int fill_grid(fgbd_ctx* ctx, int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + kBlock - 1) / kBlock, ctx->num_sms * 8));
+}
+
+int launch_expand(fgbd_ctx* ctx, const double* d_src, int64_t n, int buf) {
+  k_expand<<<fill_grid(ctx, n), kBlock, 0, ctx->stream>>>(d_src, n, (double4*)ctx->buf[buf]);
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+int launch_compact(fgbd_ctx* ctx, int64_t n, int src_buf, double* d_dst, int clip) {
+  const double4* src = src_buf >= 0 ? (const double4*)ctx->buf[src_buf] : nullptr;
+  if (clip)
+    k_compact<true><<<fill_grid(ctx, n), kBlock, 0, ctx->stream>>>(ctx->d_bufs, ctx->ctl, src, n,
+                                                                   d_dst);
+  else
+    k_compact<false><<<fill_grid(ctx, n), kBlock, 0, ctx->stream>>>(ctx->d_bufs, ctx->ctl, src, n,
+                                                                    d_dst);
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
 int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_max, int mode,
-                const uint8_t* d_inc) {
+                int early_exit, const uint8_t* d_inc) {
   MaskArgs a;
   a.fslr = ctx->fslr;
-  a.y = ctx->buf[BUF_Y];
+  a.y = (const double4*)ctx->buf[BUF_Y];
   a.inc_bytes = d_inc;
   a.n = n;
   a.thr = 2.0 * sigma_est;
@@ -328,72 +603,91 @@ int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_ma
   a.ctl = ctx->ctl;
   a.q_max = q_max;
   a.mode = mode;
+  a.early_exit = early_exit;
   a.sv2 = sigma_est * sigma_est;
   k_mask<<<red_grid(n), kBlock, 0, ctx->stream>>>(a);
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
 }
 
-int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int mode, int early_exit,
-                        double sigma_est, int w64) {
+static StepArgs step_args(fgbd_ctx* ctx, int64_t n) {
   StepArgs a{};
   a.ell = ctx->ell;
   a.w64 = ctx->w64;
-  for (int k = 0; k < 3; ++k) a.buf[k] = ctx->buf[k];
+  for (int k = 0; k < 3; ++k) a.buf[k] = (double4*)ctx->buf[k];
   a.mask = ctx->mask;
   a.n = n;
   a.part = ctx->partials;
   a.ctl = ctx->ctl;
-  a.q_max = q_max;
-  a.mode = mode;
-  a.early_exit = early_exit;
-  a.sv2 = sigma_est * sigma_est;
-  const int grid = red_grid(n);
-  for (int q = 0; q < q_max; ++q) {
-    if (w64) k_lf_step<true, true><<<grid, kBlock, 0, ctx->stream>>>(a);
-    else k_lf_step<false, true><<<grid, kBlock, 0, ctx->stream>>>(a);
-    FGBD_LAUNCH(ctx);
+  return a;
+}
+
+template <bool W64, bool SELECT, bool PIPE, int MINB, bool HINT = false>
+static int launch_persist_k(fgbd_ctx* ctx, StepArgs& a) {
+  auto kern = k_lf_persist<W64, SELECT, PIPE, MINB, HINT>;
+  const int slot = (W64 ? 1 : 0) + (SELECT ? 2 : 0) + (PIPE ? 4 : 0) + (MINB == 2 ? 8 : 0) +
+                   (HINT ? 16 : 0) + (MINB == 4 ? 32 : 0);
+  if (ctx->coop_blocks[slot] == 0) {
+    int per_sm = 0;
+    FGBD_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0));
+    ctx->coop_blocks[slot] = std::max(1, per_sm) * ctx->num_sms;
   }
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((a.n + kBlock - 1) / kBlock, ctx->coop_blocks[slot]));
+  void* args[] = {&a};
+  FGBD_CUDA(ctx, cudaLaunchCooperativeKernel((void*)kern, grid, kBlock, args, 0, ctx->stream));
+  FGBD_LAUNCH(ctx);
   return FGBD_OK;
+}
+
+// variant 2: persistent, 3 blocks/SM; 3: + slot prefetch; 4: prefetch, 2 blocks/SM
+template <bool W64, bool SELECT>
+static int launch_persist(fgbd_ctx* ctx, StepArgs& a) {
+  if (ctx->lf_variant == 3) return launch_persist_k<W64, SELECT, true, 3>(ctx, a);
+  if (ctx->lf_variant == 4) return launch_persist_k<W64, SELECT, true, 2>(ctx, a);
+  if (ctx->lf_variant == 5) return launch_persist_k<W64, SELECT, false, 3, true>(ctx, a);
+  if (ctx->lf_variant == 6) return launch_persist_k<W64, SELECT, false, 4, true>(ctx, a);
+  return launch_persist_k<W64, SELECT, false, 3>(ctx, a);
+}
+
+int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64) {
+  StepArgs a = step_args(ctx, n);
+  if (ctx->lf_variant == 0) {
+    const int grid = red_grid(n);
+    for (int q = 0; q < q_max; ++q) {
+      if (w64) k_lf_step<true, true><<<grid, kBlock, 0, ctx->stream>>>(a, 0, 0);
+      else k_lf_step<false, true><<<grid, kBlock, 0, ctx->stream>>>(a, 0, 0);
+      FGBD_LAUNCH(ctx);
+    }
+    return FGBD_OK;
+  }
+  return w64 ? launch_persist<true, true>(ctx, a) : launch_persist<false, true>(ctx, a);
 }
 
 int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf) {
-  StepArgs a{};
-  a.ell = ctx->ell;
-  a.w64 = ctx->w64;
-  a.n = n;
-  a.ctl = ctx->ctl;
-  const int grid = red_grid(n);
-  int cur = BUF_Y;
-  for (int k = 0; k < q; ++k) {
-    const int nxt = (cur == BUF_A) ? BUF_B : BUF_A;
-    a.in = ctx->buf[cur];
-    a.out = ctx->buf[nxt];
-    if (w64) k_lf_step<true, false><<<grid, kBlock, 0, ctx->stream>>>(a);
-    else k_lf_step<false, false><<<grid, kBlock, 0, ctx->stream>>>(a);
-    FGBD_LAUNCH(ctx);
-    cur = nxt;
+  *final_buf = q == 0 ? BUF_Y : ((q & 1) ? BUF_A : BUF_B);
+  if (q == 0) return FGBD_OK;
+  StepArgs a = step_args(ctx, n);
+  if (ctx->lf_variant == 0) {
+    const int grid = red_grid(n);
+    int cur = BUF_Y;
+    for (int k = 0; k < q; ++k) {
+      const int nxt = (cur == BUF_A) ? BUF_B : BUF_A;
+      if (w64) k_lf_step<true, false><<<grid, kBlock, 0, ctx->stream>>>(a, cur, nxt);
+      else k_lf_step<false, false><<<grid, kBlock, 0, ctx->stream>>>(a, cur, nxt);
+      FGBD_LAUNCH(ctx);
+      cur = nxt;
+    }
+    return FGBD_OK;
   }
-  *final_buf = cur;
-  return FGBD_OK;
-}
-
-int launch_finalize(fgbd_ctx* ctx, int64_t n, int src_buf, double* d_out) {
-  // src_buf < 0: the buffer select_q marked best (read on the device)
-  const double* src = src_buf >= 0 ? ctx->buf[src_buf] : nullptr;
-  const int64_t n3 = 3 * n;
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n3 + kBlock - 1) / kBlock,
-                                                         ctx->num_sms * 8));
-  k_finalize<<<grid, kBlock, 0, ctx->stream>>>(ctx->d_bufs, ctx->ctl, src, n3, d_out);
-  FGBD_LAUNCH(ctx);
-  return FGBD_OK;
+  a.fixed_steps = q;
+  return w64 ? launch_persist<true, false>(ctx, a) : launch_persist<false, false>(ctx, a);
 }
 
 int launch_csr_steps(fgbd_ctx* ctx, const int64_t* d_indptr, const int64_t* d_indices,
                      const double* d_w, int64_t n, const double* d_in, double* d_tmp,
                      double* d_out, int q) {
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + kBlock - 1) / kBlock,
-                                                               ctx->num_sms * 8));
+  const int grid = fill_grid(ctx, n);
   // ping-pong so that the last step lands in d_out
   const double* src = d_in;
   for (int k = 0; k < q; ++k) {

@@ -25,12 +25,23 @@
 namespace fgbd {
 
 constexpr int kNeThreads = 96;
-constexpr int kNeVals = 3 * kMom + 1;  // moments + eligible count
+constexpr int kGram = 64;                 // 8 x 8 Gram matrix per channel
+constexpr int kNeVals = 3 * kGram;        // per-block partial values
+constexpr int kRowStride = 9;             // smem patch row stride (odd: no bank conflicts)
 
-__device__ __forceinline__ int mom2_index(int k, int l) {  // k <= l, D = 7 layout
-  return 7 + k * 7 - (k * (k - 1)) / 2 + (l - k);
+// D = A(8x4) * B(4x8) + C on the fp64 tensor core.
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
 }
 
+// Block = 3 warps, warp c = colour channel c, lane = point of a 32-point
+// chunk.  Each lane builds its patch row p = (a_0-128, ..., a_{D-1}-128, 0.., 1)
+// (zeros for non-eligible points) in shared memory; the warp then adds the
+// chunk's Gram matrix P^T P to an 8x8 fp64 accumulator held in two registers
+// per lane with 8 DMMA m8n8k4 instructions.  Column 7 = 1 turns the Gram
+// matrix into [S2 S1; S1^T count]: every moment the covariance needs.
 __global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict__ meta,
                                                       const int2* __restrict__ ell,
                                                       const double* __restrict__ colors,
@@ -38,51 +49,48 @@ __global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict
                                                       double* __restrict__ fslr,
                                                       double* __restrict__ part /*[vals][grid]*/) {
   __shared__ double s_std[3][32];
+  __shared__ double s_rows[3][32 * kRowStride];
   const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double m[kMom];
-#pragma unroll
-  for (int k = 0; k < kMom; ++k) m[k] = 0.0;
-  long long elig = 0;
-  const double invD = 0.0;  // unused; divisions below are exact __ddiv_rn
-  (void)invD;
+  double* rows = s_rows[c];
+  double acc0 = 0.0, acc1 = 0.0;
   const int64_t nchunks = (n + 31) / 32;
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t i = ch * 32 + lane;
     const bool valid = i < n;
-    const uint32_t mt = valid ? meta[i] : 0u;
-    const int deg = (int)(mt & 7u);
-    const bool ok = valid && deg >= D - 1;
+    uint32_t mt = 0;
+    int nb[kSlots];
     double a[7];
 #pragma unroll
+    for (int s = 0; s < kSlots; ++s) nb[s] = 0;
+#pragma unroll
     for (int r = 0; r < 7; ++r) a[r] = 0.0;
+    if (valid) {
+      mt = meta[i];
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) nb[s] = ell[s * n + i].x;
+      a[0] = colors[4 * i + c];
+    }
+    const int deg = (int)(mt & 7u);
+    const bool ok = valid && deg >= D - 1;
     double sd = 0.0;
     if (ok) {
-      a[0] = colors[3 * i + c];
 #pragma unroll
       for (int r = 1; r < 7; ++r) {
         if (r < D) {
           const int s = (int)((mt >> (3 + 3 * (r - 1))) & 7u);
-          const int j = ell[s * n + i].x;
-          a[r] = colors[3 * (int64_t)j + c];
+          int j = nb[0];
+#pragma unroll
+          for (int t = 1; t < kSlots; ++t) j = (s == t) ? nb[t] : j;
+          a[r] = colors[4 * (int64_t)j + c];
         }
-      }
-      // shifted one-pass moments (only the first D entries are non-zero)
-      double v[7];
-#pragma unroll
-      for (int k = 0; k < 7; ++k) v[k] = (k < D) ? a[k] - 128.0 : 0.0;
-#pragma unroll
-      for (int k = 0; k < 7; ++k) {
-        m[k] += v[k];
-#pragma unroll
-        for (int l = k; l < 7; ++l) m[mom2_index(k, l)] = fma(v[k], v[l], m[mom2_index(k, l)]);
       }
       // numpy std over the patch axis: sequential sum, /D, squared
       // deviations, sequential sum, /D, sqrt -- no contraction.
-      double s = a[0];
+      double sum = a[0];
 #pragma unroll
       for (int k = 1; k < 7; ++k)
-        if (k < D) s = __dadd_rn(s, a[k]);
-      const double mean = __ddiv_rn(s, (double)D);
+        if (k < D) sum = __dadd_rn(sum, a[k]);
+      const double mean = __ddiv_rn(sum, (double)D);
       double var = 0.0;
 #pragma unroll
       for (int k = 0; k < 7; ++k) {
@@ -93,27 +101,28 @@ __global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict
       }
       sd = __dsqrt_rn(__ddiv_rn(var, (double)D));
     }
+    // patch row for the Gram update
+#pragma unroll
+    for (int k = 0; k < 7; ++k) rows[lane * kRowStride + k] = (ok && k < D) ? a[k] - 128.0 : 0.0;
+    rows[lane * kRowStride + 7] = ok ? 1.0 : 0.0;
     s_std[c][lane] = sd;
     __syncthreads();
-    if (c == 0 && valid) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const double v = rows[(4 * t + (lane & 3)) * kRowStride + (lane >> 2)];
+      dmma_884(acc0, acc1, v, v);
+    }
+    if (c == 0 && valid)
       fslr[i] = ok ? __ddiv_rn(__dadd_rn(__dadd_rn(s_std[0][lane], s_std[1][lane]),
                                          s_std[2][lane]),
                                3.0)
                    : -1.0;
-      elig += ok;
-    }
     __syncthreads();
   }
-  // per-warp (= per-channel) reduction, fixed tree
-#pragma unroll
-  for (int k = 0; k < kMom; ++k) {
-    const double t = warp_sum(m[k]);
-    if (lane == 0) part[(int64_t)(c * kMom + k) * gridDim.x + blockIdx.x] = t;
-  }
-  if (c == 0) {
-    const long long e = warp_sum_ll(elig);
-    if (lane == 0) part[(int64_t)(3 * kMom) * gridDim.x + blockIdx.x] = (double)e;
-  }
+  // lane holds G[lane>>2][(lane&3)*2 + {0,1}]
+  const int r = lane >> 2, col = (lane & 3) * 2;
+  part[(int64_t)(c * kGram + r * 8 + col) * gridDim.x + blockIdx.x] = acc0;
+  part[(int64_t)(c * kGram + r * 8 + col + 1) * gridDim.x + blockIdx.x] = acc1;
 }
 
 // out[v] = sum_b part[v][b] in a fixed tree (one block per value).
@@ -125,8 +134,8 @@ __global__ void __launch_bounds__(kBlock) k_reduce_cols(const double* __restrict
   for (int b = threadIdx.x; b < nblocks; b += blockDim.x) a[0] += part[(int64_t)v * nblocks + b];
   block_sum<1>(a, s_red);
   if (threadIdx.x == 0) {
-    if (v < 3 * kMom) ctl->mom[v / kMom][v % kMom] = a[0];
-    else ctl->eligible = (long long)a[0];
+    ctl->gram[v / kGram][v % kGram] = a[0];
+    if (v == 63) ctl->eligible = (long long)a[0];  // channel 0, G[7][7] = count
   }
 }
 
@@ -289,14 +298,15 @@ int finish_noise(fgbd_ctx* ctx, int D, int divisor, fgbd_noise* out) {
     return set_error(ctx, FGBD_E_NOISE, "need at least 2 patches, have " + std::to_string(ne));
   double sig[3];
   for (int c = 0; c < 3; ++c) {
-    const double* s1 = h.mom[c];
+    // Gram matrix of shifted patch rows: G[k][l] = sum (a_k-128)(a_l-128),
+    // G[k][7] = sum (a_k-128), G[7][7] = eligible count
+    const double* G = h.gram[c];
     double mu[7];
-    for (int k = 0; k < D; ++k) mu[k] = s1[k] / (double)ne;
+    for (int k = 0; k < D; ++k) mu[k] = G[k * 8 + 7] / (double)ne;
     double cov[7 * 7];
     for (int k = 0; k < D; ++k) {
       for (int l = k; l < D; ++l) {
-        const int idx = 7 + k * 7 - (k * (k - 1)) / 2 + (l - k);
-        const double v = h.mom[c][idx] / (double)ne - mu[k] * mu[l];
+        const double v = G[k * 8 + l] / (double)ne - mu[k] * mu[l];
         cov[k * D + l] = v;
         cov[l * D + k] = v;
       }

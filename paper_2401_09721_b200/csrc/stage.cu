@@ -31,11 +31,11 @@ __global__ void k_extract(const uint32_t* __restrict__ meta, const int2* __restr
     const int64_t p = pos[i];
     if (pidx) pidx[p] = i;
     if (!vec) continue;
-    for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D] = colors[3 * i + c];
+    for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D] = colors[4 * i + c];
     for (int r = 1; r < D; ++r) {
       const int s = (int)((mt >> (3 + 3 * (r - 1))) & 7u);
       const int64_t j = ell[s * n + i].x;
-      for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D + r] = colors[3 * j + c];
+      for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D + r] = colors[4 * j + c];
     }
   }
 }
@@ -104,10 +104,8 @@ int32_t fgbd_extract_patches(fgbd_ctx* ctx, const double* colors, int32_t D,
     cudaFree(d);
     return r;
   };
-  cudaError_t e = cudaMemcpyAsync(ctx->buf[BUF_Y], colors, 3 * n * 8,
-                                  dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                  ctx->stream);
-  if (e != cudaSuccess) return fin(cuda_error(ctx, e, "colors upload"));
+  if ((rc = upload_colors(ctx, colors, n, dev))) return fin(rc);
+  cudaError_t e;
   const int grid = (int)std::min<int64_t>((n + kBlock - 1) / kBlock, ctx->num_sms * 8);
   k_elig_flags<<<grid, kBlock, 0, ctx->stream>>>(ctx->meta, n, D, flag);
   if ((rc = scan_exclusive(ctx, flag, n, pos, tmp, total))) return fin(rc);
