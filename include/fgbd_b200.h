@@ -105,6 +105,8 @@ typedef struct fgbd_report {
   double trace[FGBD_TRACE_MAX];/* criterion at q = 0..steps */
   int32_t gpu_launches;        /* kernels launched by this call */
   double t_lf_steps;           /* seconds spent in the filter-step launches only */
+  double t_h2d;                /* coordinates host->device (colours overlap the graph build) */
+  double t_d2h;                /* denoised colours device->host */
 } fgbd_report;
 
 /* Result of NE-GBP (noise.py:63-73). */

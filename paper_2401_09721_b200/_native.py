@@ -52,7 +52,7 @@ class Report(C.Structure):
                 ("eigenvalues", (c_f64 * MAX_PATCH) * 3), ("tail_m", c_i32 * 3),
                 ("tail_tau", c_f64 * 3), ("tail_fallback", c_i32 * 3), ("n_trace", c_i32),
                 ("trace", c_f64 * TRACE_MAX), ("gpu_launches", c_i32),
-                ("t_lf_steps", c_f64)]
+                ("t_lf_steps", c_f64), ("t_h2d", c_f64), ("t_d2h", c_f64)]
 
 
 class Noise(C.Structure):
@@ -199,35 +199,70 @@ def make_config(cfg) -> Config:
     return c
 
 
+class _Lease:
+    """Returns a pinned block to its pool when the last array view dies."""
+
+    __slots__ = ("pool", "size", "ptr")
+
+    def __init__(self, pool, size, ptr):
+        self.pool, self.size, self.ptr = pool, size, ptr
+
+    def __del__(self):
+        try:
+            self.pool._release(self.size, self.ptr)
+        except Exception:
+            pass
+
+
+class PinnedPool:
+    """Recycled page-locked host blocks for device->host results.
+
+    `denoise` returns its colours in one of these blocks so the D2H copy runs
+    at full PCIe rate; the block goes back to the pool when the returned
+    array (and every view of it) is garbage-collected.  Past `max_blocks`
+    outstanding blocks it falls back to ordinary pageable memory.
+    """
+
+    def __init__(self, max_blocks: int = 16):
+        self.max_blocks = max_blocks
+        self.free: dict[int, list[int]] = {}
+        self.outstanding = 0
+        self.allocs = 0
+        self.reuses = 0
+        self.lock = threading.RLock()
+
+    def empty(self, shape, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        count = int(np.prod(shape))
+        size = max(count * dtype.itemsize, 1)
+        with self.lock:
+            lst = self.free.get(size)
+            ptr = lst.pop() if lst else None
+            if ptr is None and self.outstanding >= self.max_blocks:
+                return np.empty(shape, dtype)
+            self.outstanding += 1
+            if ptr is not None:
+                self.reuses += 1
+        if ptr is None:
+            self.allocs += 1
+            ptr = load_library().fgbd_host_alloc(size)
+            if not ptr:
+                with self.lock:
+                    self.outstanding -= 1
+                return np.empty(shape, dtype)
+        buf = (C.c_char * size).from_address(ptr)
+        buf._lease = _Lease(self, size, ptr)
+        return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
+
+    def _release(self, size, ptr):
+        with self.lock:
+            self.free.setdefault(size, []).append(ptr)
+            self.outstanding -= 1
+
+
+_pool = PinnedPool()
+
+
 def pinned_empty(shape, dtype) -> np.ndarray:
-    """numpy array backed by page-locked host memory (freed with the array)."""
-    lib = load_library()
-    dtype = np.dtype(dtype)
-    nbytes = int(np.prod(shape)) * dtype.itemsize
-    p = lib.fgbd_host_alloc(max(nbytes, 1))
-    if not p:
-        raise DeviceError("cudaMallocHost failed")
-    buf = (C.c_char * max(nbytes, 1)).from_address(p)
-    arr = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
-
-    class _Owner:
-        def __del__(self_inner):
-            try:
-                lib.fgbd_host_free(p)
-            except Exception:
-                pass
-
-    arr_owner = _Owner()
-    # keep the owner alive as long as the array (numpy base chain)
-    holder = np.ndarray.__new__(np.ndarray, arr.shape, dtype=dtype, buffer=buf)
-    holder = holder.view(_PinnedArray)
-    holder._owner = arr_owner
-    return holder
-
-
-class _PinnedArray(np.ndarray):
-    _owner = None
-
-    def __array_finalize__(self, obj):
-        if obj is not None:
-            self._owner = getattr(obj, "_owner", None)
+    """numpy array backed by recycled page-locked host memory."""
+    return _pool.empty(shape, dtype)

@@ -122,7 +122,21 @@ int upload_colors(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev) {
                                    cudaMemcpyHostToDevice, ctx->stream));
     src = ctx->out;
   }
-  return launch_expand(ctx, src, n, BUF_Y);
+  return launch_expand(ctx, src, n, BUF_Y, ctx->stream);
+}
+
+int upload_colors_async(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev) {
+  if (n <= 0) return FGBD_OK;
+  const double* src = colors;
+  if (!dev) {
+    FGBD_CUDA(ctx, cudaMemcpyAsync(ctx->out, colors, 3 * n * sizeof(double),
+                                   cudaMemcpyHostToDevice, ctx->side));
+    src = ctx->out;
+  }
+  int rc = launch_expand(ctx, src, n, BUF_Y, ctx->side);
+  if (rc) return rc;
+  FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->side));
+  return FGBD_OK;
 }
 
 int download_signal(fgbd_ctx* ctx, int src_buf, double* dst, int64_t n, bool dev, int clip) {
@@ -315,6 +329,10 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   ctx->num_sms = prop.multiProcessorCount;
   if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(e, "stream");
+  if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(e, "side stream");
+  if ((e = cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming)) != cudaSuccess)
+    return fail(e, "side event");
   for (auto& ev : ctx->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(e, "event");
   if ((e = cudaMalloc(&ctx->ctl, sizeof(Ctl))) != cudaSuccess) return fail(e, "ctl");
@@ -352,6 +370,9 @@ void fgbd_ctx_destroy(fgbd_ctx* ctx) {
   if (ctx->csr_scratch) cudaFree(ctx->csr_scratch);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
+  if (ctx->side) cudaStreamSynchronize(ctx->side);
+  if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -402,11 +423,18 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   if ((rc = ensure_capacity(ctx, n, 3 * bits > 32))) return rc;
   apply_l2_policy(ctx, n);
-  if ((rc = upload_colors(ctx, colors, n, dev))) return rc;
   if (!dev && (rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false))) return rc;
+  // the side stream starts after the coordinates have landed (full PCIe
+  // bandwidth for them) and after all earlier main-stream work on the
+  // staging buffers; it then overlaps the colour upload with the graph build
+  FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->stream));
+  FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_side, 0));
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
   if ((rc = stage_graph(ctx, dev ? coords : ctx->coords64, n, bits, true, w64))) return rc;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
+  // colours travel (and are re-laid out) while the graph is being built
+  if ((rc = upload_colors_async(ctx, colors, n, dev))) return rc;
+  FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_side, 0));
 
   fgbd_noise nz;
   std::memset(&nz, 0, sizeof(nz));
@@ -473,6 +501,8 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     rep->t_low_pass_filter = ev_sec(ev[3], ev[4]);
     rep->t_total = ev_sec(ev[0], ev[5]);
     rep->t_lf_steps = ev_sec(ev[3], ev[6]);
+    rep->t_h2d = ev_sec(ev[0], ev[1]);
+    rep->t_d2h = ev_sec(ev[4], ev[5]);
   }
   rep->gpu_launches = ctx->launches;
   return FGBD_OK;

@@ -26,6 +26,13 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
   return v;
 }
 
+// ELL slot s of point i.  Slots are stored in pairs, int4 = (nbr, payload) x 2,
+// pair-major [3][N]: a warp reads 512 contiguous bytes per pair and a row
+// needs three 16-byte loads.
+__device__ __forceinline__ int64_t eslot(int s, int64_t n, int64_t i) {
+  return (int64_t)(s >> 1) * 2 * n + 2 * i + (s & 1);
+}
+
 // Block-wide sum of NV doubles per thread; result valid in thread 0.
 // Fixed shuffle tree + fixed warp order => deterministic.
 template <int NV>
@@ -121,6 +128,14 @@ __device__ __forceinline__ int2 ld_slot_hint(const int2* p, uint64_t pol) {
   int2 v;
   asm volatile("ld.global.nc.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
                : "=r"(v.x), "=r"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ int4 ld_pair_hint(const int2* p, uint64_t pol) {
+  int4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p), "l"(pol));
   return v;
 }

@@ -90,6 +90,8 @@ struct fgbd_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;   // colour upload, overlapped with graph construction
+  cudaEvent_t ev_side = nullptr;
   int64_t cap = 0;        // points the scratch is sized for
   int key64_cap = 0;      // scratch sized for 64-bit keys
   size_t dev_bytes = 0;
@@ -155,6 +157,8 @@ int cuda_error(fgbd_ctx* ctx, cudaError_t e, const char* where);
 int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64);
 // (N,3) colours (host or device) -> BUF_Y in the (N,4) layout
 int upload_colors(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev);
+// same, issued on the side stream; the main stream waits for it at ev_side
+int upload_colors_async(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev);
 // signal buffer (src_buf < 0: the select_q best) -> (N,3) host/device array
 int download_signal(fgbd_ctx* ctx, int src_buf, double* dst, int64_t n, bool dev, int clip);
 int ensure_w64(fgbd_ctx* ctx, int64_t n);
@@ -191,7 +195,7 @@ int select_tail_host(const double* lam, int d, int divisor, int* m, double* tau,
 
 // ---- filter (filter.cu) --------------------------------------------------
 // (N,3) device colours -> signal buffer `buf` in the (N,4) layout
-int launch_expand(fgbd_ctx* ctx, const double* d_src, int64_t n, int buf);
+int launch_expand(fgbd_ctx* ctx, const double* d_src, int64_t n, int buf, cudaStream_t s);
 // signal buffer (or the select_q best buffer when src_buf < 0) -> (N,3), optional clip
 int launch_compact(fgbd_ctx* ctx, int64_t n, int src_buf, double* d_dst, int clip);
 int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_max, int mode,

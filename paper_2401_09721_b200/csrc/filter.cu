@@ -193,7 +193,7 @@ __device__ __forceinline__ double4 lf_row(const int2* __restrict__ ell,
   double w[kSlots];
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
-    const int2 sl = __ldg(&ell[s * n + i]);
+    const int2 sl = __ldg(&ell[eslot(s, n, i)]);
     nb[s] = sl.x;
     w[s] = W64 ? __ldg(&w64[s * n + i]) : (double)__int_as_float(sl.y);
   }
@@ -228,10 +228,12 @@ __device__ __forceinline__ double4 lf_row_hint(const int2* __restrict__ ell, con
   int nb[kSlots];
   double w[kSlots];
 #pragma unroll
-  for (int s = 0; s < kSlots; ++s) {
-    const int2 sl = ld_slot_hint(ell + s * n + i, pol_stream);
+  for (int s = 0; s < kSlots; s += 2) {
+    const int4 sl = ld_pair_hint(ell + eslot(s, n, i), pol_stream);
     nb[s] = sl.x;
     w[s] = (double)__int_as_float(sl.y);
+    nb[s + 1] = sl.z;
+    w[s + 1] = (double)__int_as_float(sl.w);
   }
   const double4 f = ld_row_hint(in + i, pol_keep);
   double4 g[kSlots];
@@ -291,7 +293,7 @@ __device__ __forceinline__ void load_slots(const int2* __restrict__ ell,
                                            int64_t i, int (&nb)[kSlots], double (&w)[kSlots]) {
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
-    const int2 sl = __ldg(&ell[s * n + i]);
+    const int2 sl = __ldg(&ell[eslot(s, n, i)]);
     nb[s] = sl.x;
     w[s] = W64 ? __ldg(&w64[s * n + i]) : (double)__int_as_float(sl.y);
   }
@@ -571,8 +573,8 @@ static int fill_grid(fgbd_ctx* ctx, int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + kBlock - 1) / kBlock, ctx->num_sms * 8));
 }
 
-int launch_expand(fgbd_ctx* ctx, const double* d_src, int64_t n, int buf) {
-  k_expand<<<fill_grid(ctx, n), kBlock, 0, ctx->stream>>>(d_src, n, (double4*)ctx->buf[buf]);
+int launch_expand(fgbd_ctx* ctx, const double* d_src, int64_t n, int buf, cudaStream_t s) {
+  k_expand<<<fill_grid(ctx, n), kBlock, 0, s>>>(d_src, n, (double4*)ctx->buf[buf]);
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
 }

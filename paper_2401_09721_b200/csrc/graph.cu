@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       const bool ok = s < deg;
-      ell[s * n + i] = make_int2(ok ? (int)c[s] : (int)i,
+      ell[eslot(s, n, i)] = make_int2(ok ? (int)c[s] : (int)i,
                                  (ok && !BIG) ? (int)(uint32_t)sq[s] : 0);
     }
     meta[i] = (uint32_t)deg | (order << 3);
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kBlock) k_weights(int2* __restrict__ ell,
     if (BIG) unpack(pc[i], b, &xi, &yi, &zi);
 #pragma unroll
     for (int s = 0; s < kSlots; ++s) {
-      int2 sl = ell[s * n + i];
+      int2 sl = ell[eslot(s, n, i)];
       double w = 0.0;
       if (sl.x != (int)i) {
         unsigned long long sq;
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kBlock) k_weights(int2* __restrict__ ell,
         w = exp(__ddiv_rn(-(double)sq, sg2));
       }
       sl.y = __float_as_int((float)w);
-      ell[s * n + i] = sl;
+      ell[eslot(s, n, i)] = sl;
       if (W64) w64[s * n + i] = w;
     }
   }
@@ -438,7 +438,7 @@ __global__ void k_degrees(const uint32_t* __restrict__ meta, const int2* __restr
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int dg = (int)(meta[i] & 7u);
     int up = 0;
-    for (int s = 0; s < dg; ++s) up += (ell[s * n + i].x > (int)i);
+    for (int s = 0; s < dg; ++s) up += (ell[eslot(s, n, i)].x > (int)i);
     deg[i] = dg;
     updeg[i] = up;
   }
@@ -516,7 +516,7 @@ __global__ void k_export(const uint32_t* __restrict__ meta, const int2* __restri
     int nlow = 0;
     double lo = 0.0, hi = 0.0;
     for (int s = 0; s < dg; ++s) {
-      const int j = ell[s * n + i].x;
+      const int j = ell[eslot(s, n, i)].x;
       long long xj, yj, zj;
       unpack(pc[j], b, &xj, &yj, &zj);
       const long long dx = xi - xj, dy = yi - yj, dz = zi - zj;
@@ -535,7 +535,7 @@ __global__ void k_export(const uint32_t* __restrict__ meta, const int2* __restri
         const int dj = (int)(meta[j] & 7u);
         int cnt = 0;
         for (int t = 0; t < dj; ++t) {
-          const int v = ell[t * n + j].x;
+          const int v = ell[eslot(t, n, j)].x;
           cnt += (v > j) && (v < (int)i);
         }
         eid = eoff[j] + cnt;

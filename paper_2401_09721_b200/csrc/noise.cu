@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict
     if (valid) {
       mt = meta[i];
 #pragma unroll
-      for (int s = 0; s < kSlots; ++s) nb[s] = ell[s * n + i].x;
+      for (int s = 0; s < kSlots; ++s) nb[s] = ell[eslot(s, n, i)].x;
       a[0] = colors[4 * i + c];
     }
     const int deg = (int)(mt & 7u);

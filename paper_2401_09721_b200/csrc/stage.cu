@@ -34,7 +34,7 @@ __global__ void k_extract(const uint32_t* __restrict__ meta, const int2* __restr
     for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D] = colors[4 * i + c];
     for (int r = 1; r < D; ++r) {
       const int s = (int)((mt >> (3 + 3 * (r - 1))) & 7u);
-      const int64_t j = ell[s * n + i].x;
+      const int64_t j = ell[eslot(s, n, i)].x;
       for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D + r] = colors[4 * j + c];
     }
   }

@@ -246,6 +246,8 @@ def _device_info(r: nat.Report, patch: int) -> dict:
         "gpu_launches": int(r.gpu_launches),
         "t_total": float(r.t_total),
         "t_lf_steps": float(r.t_lf_steps),
+        "t_h2d": float(r.t_h2d),
+        "t_d2h": float(r.t_d2h),
     }
 
 
@@ -273,7 +275,7 @@ def denoise(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
             raise NoiseEstimationError(f"unknown divisor rule {cfg.tau_divisor!r}")
         cfg = FilterConfig(**{**cfg.__dict__, "tau_divisor": "count"})
     ctx = nat.context()
-    out = np.empty((n, 3), np.float64)
+    out = nat.pinned_empty((n, 3), np.float64)  # full-rate D2H, recycled
     rep = nat.Report()
     cq = -1 if cached_q is None else int(cached_q)
     cs = float("nan") if cached_sigma_est is None else float(cached_sigma_est)
