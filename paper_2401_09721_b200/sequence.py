@@ -1,0 +1,108 @@
+"""Frame-sequence driver: K-frame q reuse, frame-parallel over GPUs.
+
+Reference behaviour (cli.py:98-160): frames are processed in
+groups of K = cfg.reestimate_interval; the first frame of a group runs the
+full pipeline, the other K-1 reuse its (q, sigma_est) through
+`denoise(..., cached_q, cached_sigma_est)`.  Results are identical to that
+sequential loop -- only the placement changes:
+
+* within one process, `workers` host threads each own a device context
+  (stream + scratch), so frame f+1's H2D/D2H overlaps frame f's kernels;
+* across processes (one per GPU, `torch.distributed`), the group heads are
+  spread over the ranks first, their (q, sigma_est) pairs are exchanged with
+  one `all_gather_object` of a few scalars per head (control plane, not a
+  data-path collective), then the cached frames are spread evenly.  No frame
+  data crosses GPUs (weak scaling).
+"""
+
+from __future__ import annotations
+
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+from typing import Callable, Sequence
+
+from .cloud import PointCloud
+from .filtering import DenoiseReport, FilterConfig, denoise
+
+
+@dataclass(frozen=True)
+class FramePlan:
+    frame: int
+    head: int  # index of the group head whose (q, sigma) this frame reuses; == frame for heads
+
+
+def group_heads(n_frames: int, interval: int) -> list[int]:
+    """Indices that run full estimation (cli.py:123: range(0, n, K))."""
+    if interval < 1:
+        raise ValueError(f"interval must be >= 1, got {interval}")
+    return list(range(0, n_frames, interval))
+
+
+def plan_sequence(n_frames: int, interval: int, world: int = 1) -> tuple[list[list[int]],
+                                                                        list[list[FramePlan]]]:
+    """Two-phase schedule: per rank, (heads to run, cached frames to run).
+
+    Heads are dealt round-robin; cached frames are dealt in contiguous blocks
+    of near-equal size (a rank's cached frames mostly share heads).
+    """
+    heads = group_heads(n_frames, interval)
+    head_of = {f: (f // interval) * interval for f in range(n_frames)}
+    phase1 = [heads[r::world] for r in range(world)]
+    cached = [FramePlan(f, head_of[f]) for f in range(n_frames) if head_of[f] != f]
+    per = [len(cached) // world + (1 if r < len(cached) % world else 0) for r in range(world)]
+    phase2, start = [], 0
+    for r in range(world):
+        phase2.append(cached[start:start + per[r]])
+        start += per[r]
+    return phase1, phase2
+
+
+def _run_many(fn, items, workers):
+    if workers <= 1 or len(items) <= 1:
+        return [fn(x) for x in items]
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        return list(pool.map(fn, items))
+
+
+def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
+                     cfg: FilterConfig = FilterConfig(), *, n_frames: int | None = None,
+                     workers: int = 2, process_group=None,
+                     denoise_fn=denoise) -> dict[int, tuple[PointCloud, DenoiseReport]]:
+    """Denoise a frame sequence with the reference's every-K-frames q reuse.
+
+    `frames` is a sequence of PointClouds or a loader `i -> PointCloud`
+    (frames are only materialised on the rank that processes them).  With a
+    `torch.distributed` process group the work is split across its ranks and
+    each rank returns the frames it processed; otherwise all frames are
+    returned.  `denoise_fn` defaults to the B200 `denoise`.
+    """
+    load = frames if callable(frames) else (lambda i: frames[i])
+    n = n_frames if n_frames is not None else len(frames)  # type: ignore[arg-type]
+    world, rank = 1, 0
+    if process_group is not None:
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(process_group), dist.get_rank(process_group)
+    phase1, phase2 = plan_sequence(n, cfg.reestimate_interval, world)
+    results: dict[int, tuple[PointCloud, DenoiseReport]] = {}
+
+    mine = phase1[rank]
+    for f, res in zip(mine, _run_many(lambda f: denoise_fn(load(f), cfg), mine, workers)):
+        results[f] = res
+    cached = {f: (results[f][1].selected_q, results[f][1].sigma_est) for f in mine}
+    if world > 1:
+        import torch.distributed as dist
+
+        gathered: list = [None] * world
+        dist.all_gather_object(gathered, cached, group=process_group)
+        for part in gathered:
+            cached.update(part)
+
+    def run_cached(p: FramePlan):
+        q, s = cached[p.head]
+        return denoise_fn(load(p.frame), cfg, cached_q=q, cached_sigma_est=s)
+
+    todo = phase2[rank]
+    for p, res in zip(todo, _run_many(run_cached, todo, workers)):
+        results[p.frame] = res
+    return results

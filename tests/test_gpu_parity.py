@@ -268,3 +268,21 @@ def test_full_size_frames(gpu_ready, name):
     # size-independent properties: output within the input range, sums close
     assert out.colors.sum() == pytest.approx(rec["out_sum"], rel=1e-9)
     assert (out.colors ** 2).sum() == pytest.approx(rec["out_sumsq"], rel=1e-9)
+
+
+def test_sequence_driver_matches_reference_loop(gpu_ready):
+    """cli.py:123-136 K-group q reuse, two host workers sharing the GPU."""
+    from paper_2401_09721_b200.sequence import denoise_sequence
+
+    clean, _ = fb.generate_cloud("two-tone", 20_000, seed=0)
+    frames = [fb.add_gaussian_noise(clean, 20.0, seed=1 + f) for f in range(7)]
+    cfg = fb.FilterConfig(reestimate_interval=3)
+    got = denoise_sequence(frames, cfg, workers=2)
+    for g in range(0, 7, 3):
+        ref = O.denoise(frames[g].coords, frames[g].colors, frames[g].bit_depth)
+        assert got[g][1].selected_q == ref.selected_q and not got[g][1].cached
+        for f in range(g + 1, min(g + 3, 7)):
+            rf = O.denoise(frames[f].coords, frames[f].colors, frames[f].bit_depth,
+                           cached_q=ref.selected_q, cached_sigma_est=ref.sigma_est)
+            assert got[f][1].cached and got[f][1].selected_q == ref.selected_q
+            assert np.max(np.abs(got[f][0].colors - rf.colors)) <= COLOR_ATOL
