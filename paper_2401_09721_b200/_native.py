@@ -17,7 +17,8 @@ import numpy as np
 from .errors import (CloudError, DeviceError, FilterError, GraphError,
                      NoiseEstimationError)
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libfgbd_b200.so"
+LIB_PATH = Path(os.environ.get("FGBD_LIB_PATH") or
+                Path(__file__).resolve().parent / "_lib" / "libfgbd_b200.so")
 
 FGBD_OK, E_CLOUD, E_GRAPH, E_NOISE, E_FILTER, E_CUDA, E_NCCL, E_ARG = range(8)
 FLAG_DEVICE_PTRS = 0x1

@@ -50,7 +50,7 @@ static void free_scratch(fgbd_ctx* ctx) {
     }
   f(ctx->sort.status);
   f(ctx->cand);
-  f(ctx->ell);
+  f(ctx->nbr);
   f(ctx->w64);
   f(ctx->meta);
   for (int k = 0; k < 3; ++k) {
@@ -64,7 +64,8 @@ static void free_scratch(fgbd_ctx* ctx) {
   ctx->pc = nullptr;
   ctx->sort.status = nullptr;
   ctx->cand = nullptr;
-  ctx->ell = nullptr;
+  ctx->nbr = nullptr;
+  ctx->pay = nullptr;
   ctx->w64 = nullptr;
   ctx->meta = nullptr;
   ctx->out = nullptr;
@@ -95,7 +96,8 @@ int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64) {
   FGBD_CUDA(ctx, cudaMemset(ctx->sort.status, 0, 3 * tiles * kRadix * 8));
   ctx->sort.tiles_cap = tiles;
   if ((rc = dalloc(ctx, &ctx->cand, 3 * cap))) return rc;
-  if ((rc = dalloc(ctx, &ctx->ell, kSlots * cap))) return rc;
+  if ((rc = dalloc(ctx, &ctx->nbr, 2 * kSlots * cap))) return rc;
+  ctx->pay = reinterpret_cast<uint32_t*>(ctx->nbr + 1);
   if ((rc = dalloc(ctx, &ctx->meta, cap))) return rc;
   for (int k = 0; k < 3; ++k)
     if ((rc = dalloc(ctx, &ctx->buf[k], 4 * cap))) return rc;
@@ -168,14 +170,14 @@ void apply_l2_policy(fgbd_ctx* ctx, int64_t n) {
   int max_persist = 0, max_window = 0;
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
   cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
-  const size_t bytes = (size_t)kSlots * n * sizeof(int2);
+  const size_t bytes = (size_t)2 * kSlots * n * sizeof(int);
   const size_t lim = std::min<size_t>(bytes, (size_t)max_persist);
   const size_t win = std::min<size_t>(bytes, (size_t)max_window);
   if (lim == 0 || win == 0) return;
   cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
   cudaStreamAttrValue v;
   std::memset(&v, 0, sizeof(v));
-  v.accessPolicyWindow.base_ptr = ctx->ell;
+  v.accessPolicyWindow.base_ptr = ctx->nbr;
   v.accessPolicyWindow.num_bytes = win;
   v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)lim / (float)win);
   v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -241,7 +243,8 @@ int reset_ctl(fgbd_ctx* ctx) {
 }
 
 // Load a frame's coordinates and build the weighted scan-line graph.
-int stage_graph(fgbd_ctx* ctx, const int64_t* coords, int64_t n, int bits, bool dev, int w64) {
+int stage_graph(fgbd_ctx* ctx, const int64_t* coords, int64_t n, int bits, bool dev, int w64,
+                bool weights = true) {
   int rc = ensure_capacity(ctx, n, 3 * bits > 32);
   if (rc) return rc;
   if ((rc = reset_ctl(ctx))) return rc;
@@ -252,7 +255,7 @@ int stage_graph(fgbd_ctx* ctx, const int64_t* coords, int64_t n, int bits, bool 
     ctx->cur_coords = ctx->coords64;
   }
   if ((rc = launch_graph(ctx, n, bits))) return rc;
-  return launch_weights(ctx, n, bits, w64);
+  return weights ? launch_weights(ctx, n, bits, w64) : FGBD_OK;
 }
 
 int check_graph_ctl(fgbd_ctx* ctx, int bits) {
@@ -347,6 +350,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if ((e = cudaMemset(ctx->tickets, 0, 8192 * sizeof(unsigned))) != cudaSuccess) return fail(e, "tickets");
   if (const char* v = std::getenv("FGBD_LF_VARIANT")) ctx->lf_variant = std::atoi(v);
   if (const char* v = std::getenv("FGBD_L2_PERSIST")) ctx->l2_persist = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_NE_VARIANT")) ctx->ne_variant = std::atoi(v);
   if (ensure_capacity(ctx, max_points > 0 ? max_points : 1, 0) != FGBD_OK) {
     set_error(nullptr, FGBD_E_CUDA, ctx->err);
     fgbd_ctx_destroy(ctx);
@@ -430,7 +434,9 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->stream));
   FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_side, 0));
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
-  if ((rc = stage_graph(ctx, dev ? coords : ctx->coords64, n, bits, true, w64))) return rc;
+  // the NE pass converts the ELL payloads to weights itself when it can
+  const bool fuse_w = cached_q < 0 && !w64 && bits <= 15 && ctx->ne_variant == 1;
+  if ((rc = stage_graph(ctx, dev ? coords : ctx->coords64, n, bits, true, w64, !fuse_w))) return rc;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
   // colours travel (and are re-laid out) while the graph is being built
   if ((rc = upload_colors_async(ctx, colors, n, dev))) return rc;
@@ -446,7 +452,11 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = launch_compact(ctx, n, fin, dev ? out_colors : ctx->out, 1))) return rc;
   } else {
     const int D = cfg->patch_size;
-    if ((rc = launch_noise(ctx, n, D))) return rc;
+    if ((rc = launch_noise(ctx, n, D, fuse_w ? 1 : 0))) return rc;
+    if (fuse_w) {
+      ctx->g_have_weights = 1;
+      ctx->g_weights64 = 0;
+    }
     if ((rc = pull_ctl(ctx))) return rc;
     if ((rc = check_graph_ctl(ctx, bits))) return rc;
     const int maxdeg = ctx->ctl_host->max_deg;
@@ -684,7 +694,7 @@ int32_t fgbd_estimate_noise(fgbd_ctx* ctx, const double* colors, int32_t patch_s
   const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
   int rc = upload_colors(ctx, colors, n, dev);
   if (rc) return rc;
-  if ((rc = launch_noise(ctx, n, D))) return rc;
+  if ((rc = launch_noise(ctx, n, D, 0))) return rc;
   if ((rc = pull_ctl(ctx))) return rc;
   if ((rc = finish_noise(ctx, D, tau_divisor, out))) return rc;
   if (fslr_stat_out) {

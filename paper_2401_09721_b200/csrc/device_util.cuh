@@ -26,11 +26,19 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
   return v;
 }
 
-// ELL slot s of point i.  Slots are stored in pairs, int4 = (nbr, payload) x 2,
-// pair-major [3][N]: a warp reads 512 contiguous bytes per pair and a row
-// needs three 16-byte loads.
+// The ELL graph: 6 slots per point of (neighbour, payload), payload = exact
+// squared length until the weight pass, then fp32 Gaussian weight bits.
+// Storage is one int array, slot pairs interleaved as int4 = (nbr_2p, pay_2p,
+// nbr_2p+1, pay_2p+1), pair-major [3][N]: a warp reads 512 contiguous bytes
+// per pair and a row is three 16-byte loads.  `nbr` and `pay` are strided
+// views of that array (pay = nbr + 1), both indexed by eslot().
+struct EllRef {
+  int* nbr;
+  uint32_t* pay;
+};
+
 __device__ __forceinline__ int64_t eslot(int s, int64_t n, int64_t i) {
-  return (int64_t)(s >> 1) * 2 * n + 2 * i + (s & 1);
+  return (int64_t)(s >> 1) * 4 * n + 4 * i + 2 * (s & 1);
 }
 
 // Block-wide sum of NV doubles per thread; result valid in thread 0.
@@ -132,6 +140,13 @@ __device__ __forceinline__ int2 ld_slot_hint(const int2* p, uint64_t pol) {
   return v;
 }
 
+__device__ __forceinline__ int2 ld_int2_hint(const void* p, uint64_t pol) {
+  int2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ int4 ld_pair_hint(const int2* p, uint64_t pol) {
   int4 v;
   asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"

@@ -26,6 +26,10 @@
 #include "fgbd_b200.h"
 
 namespace fgbd {
+struct EllRef;
+}
+
+namespace fgbd {
 
 constexpr int kBlock = 256;
 constexpr int kRedGrid = 148 * 4;      // fixed partition => deterministic sums
@@ -103,7 +107,8 @@ struct fgbd_ctx {
   fgbd::SortScratch sort;
   uint32_t* perm[3] = {};       // aliases into sort.vals after the last pass
   int2* cand = nullptr;         // [3][N]
-  int2* ell = nullptr;          // [6][N]
+  int* nbr = nullptr;           // ELL, interleaved int4 pairs [3][N] (see eslot)
+  uint32_t* pay = nullptr;      // = nbr + 1: payload view of the same array
   double* w64 = nullptr;        // [6][N] fp64 weights (parity mode, lazy)
   uint32_t* meta = nullptr;     // [N]
   double* buf[3] = {};          // Y, A, B signals (N,4) fp64
@@ -112,9 +117,10 @@ struct fgbd_ctx {
   uint32_t* mask = nullptr;     // [ceil(N/32)]
   double* partials = nullptr;   // reduction partials (1<<17 doubles)
   unsigned int* tickets = nullptr;  // group tickets for hierarchical reductions
-  int lf_variant = 5;           // filter-step kernel (FGBD_LF_VARIANT): 0 per-step, 2+ persistent
+  int lf_variant = 10;          // filter-step kernel (FGBD_LF_VARIANT): 0 per-step, 2+ persistent
   int coop_blocks[64] = {};      // co-resident grid of each persistent instantiation
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
+  int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)
   fgbd::Ctl* ctl = nullptr;     // device
   fgbd::Ctl* ctl_host = nullptr;  // pinned mirror
   // scratch for CSR export / injection (lazy)
@@ -186,7 +192,9 @@ int scan_exclusive(fgbd_ctx* ctx, const int64_t* in, int64_t n, int64_t* out, in
                    int64_t* d_total);
 
 // ---- noise estimation (noise.cu) ----------------------------------------
-int launch_noise(fgbd_ctx* ctx, int64_t n, int patch);
+// NE pass; fuse_weights: also convert the ELL payloads to Gaussian weights
+// (only valid before launch_weights ran and when b <= 15)
+int launch_noise(fgbd_ctx* ctx, int64_t n, int patch, int fuse_weights);
 // host side: covariance -> Jacobi -> tail -> sigma (noise.py:122-243)
 int finish_noise(fgbd_ctx* ctx, int patch, int divisor, fgbd_noise* out);
 int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err);

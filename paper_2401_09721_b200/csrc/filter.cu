@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <vector>
 
@@ -174,42 +175,80 @@ __global__ void __launch_bounds__(kBlock) k_mask(MaskArgs a) {
 // ---------------------------------------------------------------------------
 
 struct StepArgs {
-  const int2* ell;
-  const double* w64;
+  EllRef E;
+  const double* w64;    // fp64 weights [6][N] (parity mode) or null
+  const void* pc;       // packed coordinates (weights recomputed on the fly)
+  int bits;
   double4* buf[3];
   const uint32_t* mask;
   int64_t n;
   double* part;  // [2 parities][3][grid]
   Ctl* ctl;
-  int fixed_steps;  // > 0: cached path, no criterion (Y -> A/B ping-pong)
+  int fixed_steps;  // cached path: number of steps (Y -> A/B ping-pong)
 };
 
-// One random-walk step for row i (filtering.py:132-155), reference order.
-template <bool W64>
-__device__ __forceinline__ double4 lf_row(const int2* __restrict__ ell,
-                                          const double* __restrict__ w64,
-                                          const double4* in, int64_t n, int64_t i) {
-  int nb[kSlots];
-  double w[kSlots];
+// Where a row's six weights come from.
+enum WMode { W_STORED = 0, W_COORDS32 = 1, W_COORDS64 = 2 };
+
+template <typename K>
+__device__ __forceinline__ long long sqlen(K a, K b, int bits) {
+  const K m = (K(1) << bits) - 1;
+  const long long dx = (long long)(a & m) - (long long)(b & m);
+  const long long dy = (long long)((a >> bits) & m) - (long long)((b >> bits) & m);
+  const long long dz = (long long)(a >> (2 * bits)) - (long long)(b >> (2 * bits));
+  return dx * dx + dy * dy + dz * dz;
+}
+
+// Load row i's neighbours and weights.  W_STORED reads the fp32 weights the
+// weight pass stored; W_COORDS* recompute w = exp(-|g_i - g_j|^2 / sigma_g^2)
+// from the 4/8-byte packed coordinates (an L2-resident array), so the
+// per-step graph stream is only the 24-byte index row.
+template <int WM>
+__device__ __forceinline__ void load_row_slots(const StepArgs& a, int64_t i, uint64_t pol,
+                                               float neg_inv_sg2, int (&nb)[kSlots],
+                                               float (&w)[kSlots]) {
+  const int64_t n = a.n;
 #pragma unroll
-  for (int s = 0; s < kSlots; ++s) {
-    const int2 sl = __ldg(&ell[eslot(s, n, i)]);
-    nb[s] = sl.x;
-    w[s] = W64 ? __ldg(&w64[s * n + i]) : (double)__int_as_float(sl.y);
+  for (int s = 0; s < kSlots; s += 2) {
+    const int4 pr = ld_pair_hint(reinterpret_cast<const int2*>(a.E.nbr + eslot(s, n, i)), pol);
+    nb[s] = pr.x;
+    nb[s + 1] = pr.z;
+    if (WM == W_STORED) {
+      w[s] = __int_as_float(pr.y);
+      w[s + 1] = __int_as_float(pr.w);
+    }
   }
-  const double4 f = ld_row(in + i);
+  if (WM != W_STORED) {
+    using K = typename std::conditional<WM == W_COORDS32, uint32_t, unsigned long long>::type;
+    const K* pc = reinterpret_cast<const K*>(a.pc);
+    const K own = pc[i];
+    K pj[kSlots];
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) pj[s] = pc[nb[s]];
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s)
+      w[s] = nb[s] != (int)i ? __expf((float)sqlen(own, pj[s], a.bits) * neg_inv_sg2) : 0.0f;
+  }
+}
+
+// out = (d f + sum_s w_s f_s) / (2 d), the reference's order (filtering.py:132-155).
+__device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const float (&wf)[kSlots],
+                                                  const double4* in, int64_t i, uint64_t pol_keep) {
+  const double4 f = ld_row_hint(in + i, pol_keep);
   double4 g[kSlots];
 #pragma unroll
-  for (int s = 0; s < kSlots; ++s) g[s] = (w[s] != 0.0) ? ld_row(in + nb[s]) : make_double4(0, 0, 0, 0);
+  for (int s = 0; s < kSlots; ++s)
+    g[s] = (wf[s] != 0.0f) ? ld_row_hint(in + nb[s], pol_keep) : make_double4(0, 0, 0, 0);
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
-    if (nb[s] < (int)i) lo = __dadd_rn(lo, w[s]);
-    else if (nb[s] > (int)i) hi = __dadd_rn(hi, w[s]);
-    if (w[s] != 0.0) {
-      acc0 = __dadd_rn(acc0, __dmul_rn(w[s], g[s].x));
-      acc1 = __dadd_rn(acc1, __dmul_rn(w[s], g[s].y));
-      acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g[s].z));
+    const double w = (double)wf[s];
+    if (nb[s] < (int)i) lo = __dadd_rn(lo, w);
+    else if (nb[s] > (int)i) hi = __dadd_rn(hi, w);
+    if (wf[s] != 0.0f) {
+      acc0 = __dadd_rn(acc0, __dmul_rn(w, g[s].x));
+      acc1 = __dadd_rn(acc1, __dmul_rn(w, g[s].y));
+      acc2 = __dadd_rn(acc2, __dmul_rn(w, g[s].z));
     }
   }
   const double d = __dadd_rn(hi, lo);
@@ -220,35 +259,27 @@ __device__ __forceinline__ double4 lf_row(const int2* __restrict__ ell,
                       __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
 }
 
-// Same arithmetic as lf_row; ELL streamed with evict_first, signal rows
-// kept with evict_last so x_out of step q is still in L2 for step q+1.
-__device__ __forceinline__ double4 lf_row_hint(const int2* __restrict__ ell, const double4* in,
-                                               int64_t n, int64_t i, uint64_t pol_stream,
-                                               uint64_t pol_keep) {
+// fp64-weight row for the parity mode (per-step launches only).
+__device__ __forceinline__ double4 row_w64(const StepArgs& a, const double4* in, int64_t i) {
+  const int64_t n = a.n;
   int nb[kSlots];
   double w[kSlots];
 #pragma unroll
-  for (int s = 0; s < kSlots; s += 2) {
-    const int4 sl = ld_pair_hint(ell + eslot(s, n, i), pol_stream);
-    nb[s] = sl.x;
-    w[s] = (double)__int_as_float(sl.y);
-    nb[s + 1] = sl.z;
-    w[s + 1] = (double)__int_as_float(sl.w);
+  for (int s = 0; s < kSlots; ++s) {
+    nb[s] = __ldg(a.E.nbr + eslot(s, n, i));
+    w[s] = __ldg(&a.w64[s * n + i]);
   }
-  const double4 f = ld_row_hint(in + i, pol_keep);
-  double4 g[kSlots];
-#pragma unroll
-  for (int s = 0; s < kSlots; ++s)
-    g[s] = (w[s] != 0.0) ? ld_row_hint(in + nb[s], pol_keep) : make_double4(0, 0, 0, 0);
+  const double4 f = ld_row(in + i);
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
     if (nb[s] < (int)i) lo = __dadd_rn(lo, w[s]);
     else if (nb[s] > (int)i) hi = __dadd_rn(hi, w[s]);
     if (w[s] != 0.0) {
-      acc0 = __dadd_rn(acc0, __dmul_rn(w[s], g[s].x));
-      acc1 = __dadd_rn(acc1, __dmul_rn(w[s], g[s].y));
-      acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g[s].z));
+      const double4 g = ld_row(in + nb[s]);
+      acc0 = __dadd_rn(acc0, __dmul_rn(w[s], g.x));
+      acc1 = __dadd_rn(acc1, __dmul_rn(w[s], g.y));
+      acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g.z));
     }
   }
   const double d = __dadd_rn(hi, lo);
@@ -285,57 +316,65 @@ __device__ __forceinline__ void select_update(SelState& s, double crit, int q_ma
   s.out_b = nout;
 }
 
-// Row kernel with the next row's ELL slots prefetched while the current
-// row's neighbour gathers are in flight (software pipelining).
-template <bool W64>
-__device__ __forceinline__ void load_slots(const int2* __restrict__ ell,
-                                           const double* __restrict__ w64, int64_t n,
-                                           int64_t i, int (&nb)[kSlots], double (&w)[kSlots]) {
-#pragma unroll
-  for (int s = 0; s < kSlots; ++s) {
-    const int2 sl = __ldg(&ell[eslot(s, n, i)]);
-    nb[s] = sl.x;
-    w[s] = W64 ? __ldg(&w64[s * n + i]) : (double)__int_as_float(sl.y);
-  }
+__device__ __forceinline__ double4* pick_buf(const StepArgs& a, int b) {
+  return b == 0 ? a.buf[0] : (b == 1 ? a.buf[1] : a.buf[2]);
 }
 
-template <bool W64>
-__device__ __forceinline__ double4 lf_row_pre(const int (&nb)[kSlots], const double (&w)[kSlots],
-                                              const double4* in, int64_t i) {
-  const double4 f = ld_row(in + i);
-  double4 g[kSlots];
+// One sweep of this block's rows: out = P in, optionally summing out^2 over
+// included rows.  The next row's graph slots are fetched while the current
+// row's neighbour gathers are in flight.
+template <int WM, bool SUMS>
+__device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, double4* out,
+                                      bool mask_all, float neg_inv_sg2, double (&sx)[3]) {
+  const int64_t n = a.n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int nbc[kSlots], nbn[kSlots];
+  float wc[kSlots], wn[kSlots];
+  if (i < n) load_row_slots<WM>(a, i, pol_stream, neg_inv_sg2, nbn, wn);
+  while (i < n) {
 #pragma unroll
-  for (int s = 0; s < kSlots; ++s) g[s] = (w[s] != 0.0) ? ld_row(in + nb[s]) : make_double4(0, 0, 0, 0);
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
-#pragma unroll
-  for (int s = 0; s < kSlots; ++s) {
-    if (nb[s] < (int)i) lo = __dadd_rn(lo, w[s]);
-    else if (nb[s] > (int)i) hi = __dadd_rn(hi, w[s]);
-    if (w[s] != 0.0) {
-      acc0 = __dadd_rn(acc0, __dmul_rn(w[s], g[s].x));
-      acc1 = __dadd_rn(acc1, __dmul_rn(w[s], g[s].y));
-      acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g[s].z));
+    for (int s = 0; s < kSlots; ++s) {
+      nbc[s] = nbn[s];
+      wc[s] = wn[s];
     }
+    const int64_t inext = i + stride;
+    if (inext < n) load_row_slots<WM>(a, inext, pol_stream, neg_inv_sg2, nbn, wn);
+    const double4 o = row_from_slots(nbc, wc, in, i, pol_keep);
+    st_row_hint(out + i, o, pol_keep);
+    if (SUMS && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+      sx[0] = fma(o.x, o.x, sx[0]);
+      sx[1] = fma(o.y, o.y, sx[1]);
+      sx[2] = fma(o.z, o.z, sx[2]);
+    }
+    i = inext;
   }
-  const double d = __dadd_rn(hi, lo);
-  if (d == 0.0) return f;
-  const double d2 = __dmul_rn(2.0, d);
-  return make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
-                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
-                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
 }
 
-template <bool W64, bool SELECT, bool PIPE, int MINB, bool HINT = false>
-__global__ void __launch_bounds__(kBlock, MINB) k_lf_persist(StepArgs a) {
+// The whole filter-step loop in ONE cooperative launch.
+//
+// SELECT = false: the cached path (filtering.py:313-326), fixed_steps steps
+// ping-ponging Y -> A -> B -> A ...
+//
+// SELECT = true: select_q with the decision lagged by one step.  At the top
+// of iteration c, x_c is complete (buffer in_b) and decisions are known up to
+// c-1.  The block sweeps step c+1 into the buffer that is neither x_c's nor
+// the best-so-far's (both known without crit_c, so the rotation is safe),
+// THEN reduces step c's partials and decides -- the reduction overlaps the
+// wait for the slowest block at the next grid barrier.  Every block reduces
+// the same partials in the same order, so all reach the same decision.  A
+// stop decided at c discards the speculative x_{c+1}; q_max stops never
+// compute it.
+template <int WM, bool SELECT>
+__global__ void __launch_bounds__(kBlock, 3) k_lf_run(StepArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double s_red[32 * 3];
-  // select_q state is block-uniform: thread 0 owns it, the block reads it
   __shared__ SelState s_st;
   __shared__ double s_sy[3], s_sv2;
   __shared__ long long s_inc;
   __shared__ int s_qmax, s_mode, s_early, s_mask_all;
   Ctl* ctl = a.ctl;
-  const int64_t n = a.n;
   const int nb = gridDim.x;
   if (threadIdx.x == 0) {
     if (SELECT) {
@@ -356,85 +395,55 @@ __global__ void __launch_bounds__(kBlock, MINB) k_lf_persist(StepArgs a) {
   }
   __syncthreads();
   const bool mask_all = s_mask_all != 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  float neg_inv_sg2 = 0.0f;
+  if (WM != W_STORED) {
+    const double sg = ctl->sigma_g;
+    neg_inv_sg2 = (float)(-1.0 / (sg * sg));
+  }
+  int c = s_st.q;  // x_c complete and decided (c = 0 at entry)
+  bool decided = true;
   while (!s_st.stop) {
-    const int ib = s_st.in_b, ob = s_st.out_b, q = s_st.q;
-    const double4* in = ib == 0 ? a.buf[0] : (ib == 1 ? a.buf[1] : a.buf[2]);
-    double4* out = ob == 0 ? a.buf[0] : (ob == 1 ? a.buf[1] : a.buf[2]);
-    double sx[3] = {0.0, 0.0, 0.0};
-    if (HINT && !W64) {
-      const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
-      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const double4 o = lf_row_hint(a.ell, in, n, i, pol_stream, pol_keep);
-        st_row_hint(out + i, o, pol_keep);
-        if (SELECT && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
-          sx[0] = fma(o.x, o.x, sx[0]);
-          sx[1] = fma(o.y, o.y, sx[1]);
-          sx[2] = fma(o.z, o.z, sx[2]);
-        }
-      }
-    } else if (PIPE) {
-      int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-      int nbr[kSlots], nbn[kSlots];
-      double w[kSlots], wn[kSlots];
-      if (i < n) load_slots<W64>(a.ell, a.w64, n, i, nbn, wn);
-      while (i < n) {
-#pragma unroll
-        for (int s = 0; s < kSlots; ++s) {
-          nbr[s] = nbn[s];
-          w[s] = wn[s];
-        }
-        const int64_t inext = i + stride;
-        if (inext < n) load_slots<W64>(a.ell, a.w64, n, inext, nbn, wn);
-        const double4 o = lf_row_pre<W64>(nbr, w, in, i);
-        st_row(out + i, o);
-        if (SELECT && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
-          sx[0] = fma(o.x, o.x, sx[0]);
-          sx[1] = fma(o.y, o.y, sx[1]);
-          sx[2] = fma(o.z, o.z, sx[2]);
-        }
-        i = inext;
-      }
-    } else {
-      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const double4 o = lf_row<W64>(a.ell, a.w64, in, n, i);
-        st_row(out + i, o);
-        if (SELECT && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
-          sx[0] = fma(o.x, o.x, sx[0]);
-          sx[1] = fma(o.y, o.y, sx[1]);
-          sx[2] = fma(o.z, o.z, sx[2]);
-        }
+    const int ib = s_st.in_b, bb = s_st.best_b;
+    int ob = BUF_A;
+    if (ob == ib || ob == bb) ob = BUF_B;
+    if (ob == ib || ob == bb) ob = BUF_Y;
+    if (c < s_qmax) {
+      double sx[3] = {0.0, 0.0, 0.0};
+      sweep<WM, SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx);
+      if (SELECT) {
+        block_sum<3>(sx, s_red);
+        if (threadIdx.x == 0)
+          for (int k = 0; k < 3; ++k) a.part[((c + 1) & 1) * 3 * nb + k * nb + blockIdx.x] = sx[k];
       }
     }
-    double* part = a.part + (q & 1) * 3 * nb;
-    if (SELECT) {
-      block_sum<3>(sx, s_red);
-      if (threadIdx.x == 0)
-        for (int k = 0; k < 3; ++k) part[k * nb + blockIdx.x] = sx[k];
-    }
-    grid.sync();
-    if (SELECT) {
-      // every block reduces the same partials in the same order -> the
-      // same criterion bits and the same decision everywhere
+    if (SELECT && !decided) {
+      const double* part = a.part + (c & 1) * 3 * nb;
       double t[3] = {0.0, 0.0, 0.0};
       for (int b = threadIdx.x; b < nb; b += blockDim.x)
 #pragma unroll
         for (int k = 0; k < 3; ++k) t[k] += __ldcg(&part[k * nb + b]);
-      block_sum<3>(t, s_red);  // ends with __syncthreads
+      block_sum<3>(t, s_red);
       if (threadIdx.x == 0) {
         const double crit = criterion(s_sy, t, s_inc, s_sv2, s_mode);
+        s_st.out_b = s_st.in_b;  // x_c's buffer becomes the best if crit_c improves
+        s_st.q = c - 1;
         select_update(s_st, crit, s_qmax, s_early);
-        if (blockIdx.x == 0 && s_st.q < FGBD_TRACE_MAX) ctl->trace[s_st.q] = crit;
+        if (blockIdx.x == 0 && c < FGBD_TRACE_MAX) ctl->trace[c] = crit;
       }
-    } else if (threadIdx.x == 0) {
-      s_st.q += 1;
-      s_st.stop = s_st.q >= s_qmax;
-      const int nin = s_st.out_b;
-      s_st.out_b = (nin == BUF_A) ? BUF_B : BUF_A;
-      s_st.in_b = nin;
-      s_st.best_b = nin;
+      __syncthreads();
+    }
+    if (!SELECT && c >= s_qmax) break;
+    if (s_st.stop) break;
+    grid.sync();
+    if (threadIdx.x == 0) {
+      s_st.in_b = ob;
+      s_st.out_b = ob;
+      s_st.q = c + 1;
+      if (!SELECT) s_st.best_b = ob;
     }
     __syncthreads();
+    c += 1;
+    decided = false;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ctl->q = s_st.q;
@@ -443,14 +452,13 @@ __global__ void __launch_bounds__(kBlock, MINB) k_lf_persist(StepArgs a) {
     ctl->best_crit = s_st.best_crit;
     ctl->best_buf = s_st.best_b;
     ctl->in_buf = s_st.in_b;
-    ctl->out_buf = s_st.out_b;
     ctl->streak = s_st.streak;
     ctl->prev_crit = s_st.prev;
     ctl->stop = 1;
   }
 }
 
-// Variant 0: one step per launch (grid-stride rows, last-block decision).
+// Variant 0 / parity mode: one step per launch, last-block decision.
 template <bool W64, bool SELECT>
 __global__ void __launch_bounds__(kBlock) k_lf_step(StepArgs a, int fin, int fout) {
   __shared__ double s_red[32 * 3];
@@ -461,18 +469,27 @@ __global__ void __launch_bounds__(kBlock) k_lf_step(StepArgs a, int fin, int fou
   bool mask_all = true;
   if (SELECT) {
     if (*(volatile int*)&ctl->stop) return;
-    in = a.buf[ctl->in_buf];
-    out = a.buf[ctl->out_buf];
+    in = pick_buf(a, ctl->in_buf);
+    out = pick_buf(a, ctl->out_buf);
     mask_all = ctl->mask_all != 0;
   } else {
-    in = a.buf[fin];
-    out = a.buf[fout];
+    in = pick_buf(a, fin);
+    out = pick_buf(a, fout);
   }
   const int64_t n = a.n;
   double sx[3] = {0.0, 0.0, 0.0};
+  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const double4 o = lf_row<W64>(a.ell, a.w64, in, n, i);
+    double4 o;
+    if (W64) {
+      o = row_w64(a, in, i);
+    } else {
+      int nbr[kSlots];
+      float w[kSlots];
+      load_row_slots<W_STORED>(a, i, pol_stream, 0.0f, nbr, w);
+      o = row_from_slots(nbr, w, in, i, pol_keep);
+    }
     st_row(out + i, o);
     if (SELECT && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
       sx[0] = fma(o.x, o.x, sx[0]);
@@ -614,8 +631,10 @@ int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_ma
 
 static StepArgs step_args(fgbd_ctx* ctx, int64_t n) {
   StepArgs a{};
-  a.ell = ctx->ell;
+  a.E = EllRef{ctx->nbr, ctx->pay};
   a.w64 = ctx->w64;
+  a.pc = ctx->pc;
+  a.bits = ctx->g_bits;
   for (int k = 0; k < 3; ++k) a.buf[k] = (double4*)ctx->buf[k];
   a.mask = ctx->mask;
   a.n = n;
@@ -624,11 +643,10 @@ static StepArgs step_args(fgbd_ctx* ctx, int64_t n) {
   return a;
 }
 
-template <bool W64, bool SELECT, bool PIPE, int MINB, bool HINT = false>
-static int launch_persist_k(fgbd_ctx* ctx, StepArgs& a) {
-  auto kern = k_lf_persist<W64, SELECT, PIPE, MINB, HINT>;
-  const int slot = (W64 ? 1 : 0) + (SELECT ? 2 : 0) + (PIPE ? 4 : 0) + (MINB == 2 ? 8 : 0) +
-                   (HINT ? 16 : 0) + (MINB == 4 ? 32 : 0);
+template <int WM, bool SELECT>
+static int launch_run(fgbd_ctx* ctx, StepArgs& a) {
+  auto kern = k_lf_run<WM, SELECT>;
+  const int slot = WM * 2 + (SELECT ? 1 : 0);
   if (ctx->coop_blocks[slot] == 0) {
     int per_sm = 0;
     FGBD_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0));
@@ -642,19 +660,19 @@ static int launch_persist_k(fgbd_ctx* ctx, StepArgs& a) {
   return FGBD_OK;
 }
 
-// variant 2: persistent, 3 blocks/SM; 3: + slot prefetch; 4: prefetch, 2 blocks/SM
-template <bool W64, bool SELECT>
-static int launch_persist(fgbd_ctx* ctx, StepArgs& a) {
-  if (ctx->lf_variant == 3) return launch_persist_k<W64, SELECT, true, 3>(ctx, a);
-  if (ctx->lf_variant == 4) return launch_persist_k<W64, SELECT, true, 2>(ctx, a);
-  if (ctx->lf_variant == 5) return launch_persist_k<W64, SELECT, false, 3, true>(ctx, a);
-  if (ctx->lf_variant == 6) return launch_persist_k<W64, SELECT, false, 4, true>(ctx, a);
-  return launch_persist_k<W64, SELECT, false, 3>(ctx, a);
+// Weight source for the persistent kernels: variant 11 recomputes them from
+// the packed coordinates, otherwise the stored fp32 weights are read.
+template <bool SELECT>
+static int launch_run_any(fgbd_ctx* ctx, StepArgs& a) {
+  if (ctx->lf_variant == 11)
+    return 3 * ctx->g_bits <= 32 ? launch_run<W_COORDS32, SELECT>(ctx, a)
+                                 : launch_run<W_COORDS64, SELECT>(ctx, a);
+  return launch_run<W_STORED, SELECT>(ctx, a);
 }
 
 int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64) {
   StepArgs a = step_args(ctx, n);
-  if (ctx->lf_variant == 0) {
+  if (ctx->lf_variant == 0 || w64) {
     const int grid = red_grid(n);
     for (int q = 0; q < q_max; ++q) {
       if (w64) k_lf_step<true, true><<<grid, kBlock, 0, ctx->stream>>>(a, 0, 0);
@@ -663,14 +681,14 @@ int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64) {
     }
     return FGBD_OK;
   }
-  return w64 ? launch_persist<true, true>(ctx, a) : launch_persist<false, true>(ctx, a);
+  return launch_run_any<true>(ctx, a);
 }
 
 int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf) {
   *final_buf = q == 0 ? BUF_Y : ((q & 1) ? BUF_A : BUF_B);
   if (q == 0) return FGBD_OK;
   StepArgs a = step_args(ctx, n);
-  if (ctx->lf_variant == 0) {
+  if (ctx->lf_variant == 0 || w64) {
     const int grid = red_grid(n);
     int cur = BUF_Y;
     for (int k = 0; k < q; ++k) {
@@ -683,7 +701,7 @@ int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf)
     return FGBD_OK;
   }
   a.fixed_steps = q;
-  return w64 ? launch_persist<true, false>(ctx, a) : launch_persist<false, false>(ctx, a);
+  return launch_run_any<false>(ctx, a);
 }
 
 int launch_csr_steps(fgbd_ctx* ctx, const int64_t* d_indptr, const int64_t* d_indices,

@@ -305,7 +305,7 @@ __device__ __forceinline__ void sort6(unsigned (&c)[6]) {
 template <typename K, bool BIG>
 __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
                                                  const K* __restrict__ pc, int64_t n, int b,
-                                                 int2* __restrict__ ell,
+                                                 EllRef ell,
                                                  uint32_t* __restrict__ meta,
                                                  double* __restrict__ partials,
                                                  Ctl* __restrict__ ctl) {
@@ -361,8 +361,8 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       const bool ok = s < deg;
-      ell[eslot(s, n, i)] = make_int2(ok ? (int)c[s] : (int)i,
-                                 (ok && !BIG) ? (int)(uint32_t)sq[s] : 0);
+      ell.nbr[eslot(s, n, i)] = ok ? (int)c[s] : (int)i;
+      ell.pay[eslot(s, n, i)] = (ok && !BIG) ? (uint32_t)sq[s] : 0u;
     }
     meta[i] = (uint32_t)deg | (order << 3);
     maxdeg = max(maxdeg, deg);
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
 // Eq. (4): w = exp(-sqdist / sigma_g^2).  fp64 evaluation, fp32 storage in
 // the slot payload (and fp64 copy in parity mode).
 template <typename K, bool BIG, bool W64>
-__global__ void __launch_bounds__(kBlock) k_weights(int2* __restrict__ ell,
+__global__ void __launch_bounds__(kBlock) k_weights(EllRef ell,
                                                     double* __restrict__ w64,
                                                     const K* __restrict__ pc, int64_t n,
                                                     int b, const Ctl* __restrict__ ctl) {
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kBlock) k_weights(int2* __restrict__ ell,
     if (BIG) unpack(pc[i], b, &xi, &yi, &zi);
 #pragma unroll
     for (int s = 0; s < kSlots; ++s) {
-      int2 sl = ell[eslot(s, n, i)];
+      int2 sl = make_int2(ell.nbr[eslot(s, n, i)], (int)ell.pay[eslot(s, n, i)]);
       double w = 0.0;
       if (sl.x != (int)i) {
         unsigned long long sq;
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kBlock) k_weights(int2* __restrict__ ell,
         w = exp(__ddiv_rn(-(double)sq, sg2));
       }
       sl.y = __float_as_int((float)w);
-      ell[eslot(s, n, i)] = sl;
+      ell.pay[eslot(s, n, i)] = (uint32_t)sl.y;
       if (W64) w64[s * n + i] = w;
     }
   }
@@ -432,13 +432,13 @@ __global__ void __launch_bounds__(kBlock) k_weights(int2* __restrict__ ell,
 // CSR export (reference conventions)
 // ---------------------------------------------------------------------------
 
-__global__ void k_degrees(const uint32_t* __restrict__ meta, const int2* __restrict__ ell,
+__global__ void k_degrees(const uint32_t* __restrict__ meta, const int* __restrict__ ell,
                           int64_t n, int64_t* __restrict__ deg, int64_t* __restrict__ updeg) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int dg = (int)(meta[i] & 7u);
     int up = 0;
-    for (int s = 0; s < dg; ++s) up += (ell[eslot(s, n, i)].x > (int)i);
+    for (int s = 0; s < dg; ++s) up += (ell[eslot(s, n, i)] > (int)i);
     deg[i] = dg;
     updeg[i] = up;
   }
@@ -494,7 +494,7 @@ __global__ void k_scan_apply(const int64_t* __restrict__ in, int64_t n,
 }
 
 template <typename K>
-__global__ void k_export(const uint32_t* __restrict__ meta, const int2* __restrict__ ell,
+__global__ void k_export(const uint32_t* __restrict__ meta, const int* __restrict__ ell,
                          const K* __restrict__ pc, int64_t n, int b,
                          const int64_t* __restrict__ rowoff, const int64_t* __restrict__ eoff,
                          const Ctl* __restrict__ ctl, int64_t* __restrict__ indptr,
@@ -516,7 +516,7 @@ __global__ void k_export(const uint32_t* __restrict__ meta, const int2* __restri
     int nlow = 0;
     double lo = 0.0, hi = 0.0;
     for (int s = 0; s < dg; ++s) {
-      const int j = ell[eslot(s, n, i)].x;
+      const int j = ell[eslot(s, n, i)];
       long long xj, yj, zj;
       unpack(pc[j], b, &xj, &yj, &zj);
       const long long dx = xi - xj, dy = yi - yj, dz = zi - zj;
@@ -535,7 +535,7 @@ __global__ void k_export(const uint32_t* __restrict__ meta, const int2* __restri
         const int dj = (int)(meta[j] & 7u);
         int cnt = 0;
         for (int t = 0; t < dj; ++t) {
-          const int v = ell[eslot(t, n, j)].x;
+          const int v = ell[eslot(t, n, j)];
           cnt += (v > j) && (v < (int)i);
         }
         eid = eoff[j] + cnt;
@@ -643,11 +643,11 @@ static int graph_impl(fgbd_ctx* ctx, int64_t n, int b) {
   const int grid = grid_for(n, kRedGrid);
   if (b > 15) {
     k_rows<K, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b,
-                                                      ctx->ell, ctx->meta, ctx->partials,
+                                                      EllRef{ctx->nbr, ctx->pay}, ctx->meta, ctx->partials,
                                                       ctx->ctl);
   } else {
     k_rows<K, false><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b,
-                                                       ctx->ell, ctx->meta, ctx->partials,
+                                                       EllRef{ctx->nbr, ctx->pay}, ctx->meta, ctx->partials,
                                                        ctx->ctl);
   }
   FGBD_LAUNCH(ctx);
@@ -671,14 +671,14 @@ static int weights_impl(fgbd_ctx* ctx, int64_t n, int b, int w64) {
   const K* pc = (const K*)ctx->pc;
   if (b > 15) {
     if (w64)
-      k_weights<K, true, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->ell, ctx->w64, pc, n, b, ctx->ctl);
+      k_weights<K, true, true><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->ctl);
     else
-      k_weights<K, true, false><<<grid, kBlock, 0, ctx->stream>>>(ctx->ell, ctx->w64, pc, n, b, ctx->ctl);
+      k_weights<K, true, false><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->ctl);
   } else {
     if (w64)
-      k_weights<K, false, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->ell, ctx->w64, pc, n, b, ctx->ctl);
+      k_weights<K, false, true><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->ctl);
     else
-      k_weights<K, false, false><<<grid, kBlock, 0, ctx->stream>>>(ctx->ell, ctx->w64, pc, n, b, ctx->ctl);
+      k_weights<K, false, false><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->ctl);
   }
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
@@ -767,7 +767,7 @@ int launch_export(fgbd_ctx* ctx, int64_t n, int64_t* d_indptr, int64_t* d_indice
   int64_t* t2 = t1 + tiles;
   int64_t* totals = t2 + tiles;
   const int grid = grid_for(n, ctx->num_sms * 8);
-  k_degrees<<<grid, kBlock, 0, ctx->stream>>>(ctx->meta, ctx->ell, n, deg, updeg);
+  k_degrees<<<grid, kBlock, 0, ctx->stream>>>(ctx->meta, ctx->nbr, n, deg, updeg);
   FGBD_LAUNCH(ctx);
   int rc = scan_exclusive(ctx, deg, n, rowoff, t1, totals);
   if (rc) return rc;
@@ -775,11 +775,11 @@ int launch_export(fgbd_ctx* ctx, int64_t n, int64_t* d_indptr, int64_t* d_indice
   if (rc) return rc;
   if (3 * ctx->g_bits <= 32)
     k_export<uint32_t><<<grid, kBlock, 0, ctx->stream>>>(
-        ctx->meta, ctx->ell, (const uint32_t*)ctx->pc, n, ctx->g_bits, rowoff, eoff, ctx->ctl,
+        ctx->meta, ctx->nbr, (const uint32_t*)ctx->pc, n, ctx->g_bits, rowoff, eoff, ctx->ctl,
         d_indptr, d_indices, d_csr_edge, d_edge_u, d_edge_v, d_sqdist, d_weights, d_wdeg);
   else
     k_export<unsigned long long><<<grid, kBlock, 0, ctx->stream>>>(
-        ctx->meta, ctx->ell, (const unsigned long long*)ctx->pc, n, ctx->g_bits, rowoff, eoff,
+        ctx->meta, ctx->nbr, (const unsigned long long*)ctx->pc, n, ctx->g_bits, rowoff, eoff,
         ctx->ctl, d_indptr, d_indices, d_csr_edge, d_edge_u, d_edge_v, d_sqdist, d_weights,
         d_wdeg);
   FGBD_LAUNCH(ctx);

@@ -43,7 +43,7 @@ __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, doubl
 // per lane with 8 DMMA m8n8k4 instructions.  Column 7 = 1 turns the Gram
 // matrix into [S2 S1; S1^T count]: every moment the covariance needs.
 __global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict__ meta,
-                                                      const int2* __restrict__ ell,
+                                                      const int* __restrict__ ell,
                                                       const double* __restrict__ colors,
                                                       int64_t n, int D,
                                                       double* __restrict__ fslr,
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict
     if (valid) {
       mt = meta[i];
 #pragma unroll
-      for (int s = 0; s < kSlots; ++s) nb[s] = ell[eslot(s, n, i)].x;
+      for (int s = 0; s < kSlots; ++s) nb[s] = ell[eslot(s, n, i)];
       a[0] = colors[4 * i + c];
     }
     const int deg = (int)(mt & 7u);
@@ -125,6 +125,132 @@ __global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict
   part[(int64_t)(c * kGram + r * 8 + col + 1) * gridDim.x + blockIdx.x] = acc1;
 }
 
+// One thread per point, all three channels: one 256-bit gather per patch
+// neighbour; per warp, three 8x8 Gram accumulators on the DMMA tensor core
+// (one per channel, 2 registers each).  With WEIGHTS the kernel also turns
+// the ELL payload (exact squared length) into the fp32 Gaussian weight --
+// the rows are being read here anyway, so Eq. (4) costs no extra pass.
+constexpr int kNe2Warps = 4;
+
+__device__ __forceinline__ double ch(const double4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : v.z);
+}
+
+__device__ __forceinline__ double patch_std(const double4 (&v)[7], int c, int D) {
+  double sum = ch(v[0], c);
+#pragma unroll
+  for (int k = 1; k < 7; ++k)
+    if (k < D) sum = __dadd_rn(sum, ch(v[k], c));
+  const double mean = __ddiv_rn(sum, (double)D);
+  double var = 0.0;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    if (k < D) {
+      const double dv = __dadd_rn(ch(v[k], c), -mean);
+      var = __dadd_rn(var, __dmul_rn(dv, dv));
+    }
+  }
+  return __dsqrt_rn(__ddiv_rn(var, (double)D));
+}
+
+template <bool WEIGHTS>
+__global__ void __launch_bounds__(kNe2Warps * 32) k_noise2(const uint32_t* __restrict__ meta,
+                                                           EllRef ell,
+                                                           const double4* __restrict__ colors,
+                                                           int64_t n, int D,
+                                                           const Ctl* __restrict__ ctl,
+                                                           double* __restrict__ fslr,
+                                                           double* __restrict__ part) {
+  __shared__ double s_rows[kNe2Warps][32 * kRowStride];
+  __shared__ double s_acc[kNe2Warps][3][kGram];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* rows = s_rows[warp];
+  double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  double sg2 = 1.0;
+  if (WEIGHTS) {
+    const double sg = ctl->sigma_g;
+    sg2 = sg * sg;
+  }
+  const int64_t nchunks = (n + 31) / 32;
+  const int64_t wstride = (int64_t)gridDim.x * kNe2Warps;
+  for (int64_t chk = (int64_t)blockIdx.x * kNe2Warps + warp; chk < nchunks; chk += wstride) {
+    const int64_t i = chk * 32 + lane;
+    const bool valid = i < n;
+    uint32_t mt = 0;
+    int nb[kSlots];
+    double4 v[7];
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) nb[s] = 0;
+#pragma unroll
+    for (int r = 0; r < 7; ++r) v[r] = make_double4(0, 0, 0, 0);
+    if (valid) {
+      mt = meta[i];
+#pragma unroll
+      for (int s = 0; s < kSlots; s += 2) {
+        int4 pr = *reinterpret_cast<const int4*>(ell.nbr + eslot(s, n, i));
+        nb[s] = pr.x;
+        nb[s + 1] = pr.z;
+        if (WEIGHTS) {
+          const double w0 = pr.x != (int)i ? exp(__ddiv_rn(-(double)(uint32_t)pr.y, sg2)) : 0.0;
+          const double w1 = pr.z != (int)i ? exp(__ddiv_rn(-(double)(uint32_t)pr.w, sg2)) : 0.0;
+          pr.y = __float_as_int((float)w0);
+          pr.w = __float_as_int((float)w1);
+          *reinterpret_cast<int4*>(ell.nbr + eslot(s, n, i)) = pr;
+        }
+      }
+      v[0] = ld_row(colors + i);
+    }
+    const int deg = (int)(mt & 7u);
+    const bool ok = valid && deg >= D - 1;
+    if (ok) {
+#pragma unroll
+      for (int r = 1; r < 7; ++r) {
+        if (r < D) {
+          const int s = (int)((mt >> (3 + 3 * (r - 1))) & 7u);
+          int j = nb[0];
+#pragma unroll
+          for (int t = 1; t < kSlots; ++t) j = (s == t) ? nb[t] : j;
+          v[r] = ld_row(colors + j);
+        }
+      }
+    }
+    if (valid) {
+      // numpy std over the patch axis per channel, then the channel mean
+      fslr[i] = ok ? __ddiv_rn(__dadd_rn(__dadd_rn(patch_std(v, 0, D), patch_std(v, 1, D)),
+                                         patch_std(v, 2, D)),
+                               3.0)
+                   : -1.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+      for (int k = 0; k < 7; ++k)
+        rows[lane * kRowStride + k] = (ok && k < D) ? ch(v[k], c) - 128.0 : 0.0;
+      rows[lane * kRowStride + 7] = ok ? 1.0 : 0.0;
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const double x = rows[(4 * t + (lane & 3)) * kRowStride + (lane >> 2)];
+        dmma_884(acc[c][0], acc[c][1], x, x);
+      }
+      __syncwarp();
+    }
+  }
+  const int r = lane >> 2, col = (lane & 3) * 2;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    s_acc[warp][c][r * 8 + col] = acc[c][0];
+    s_acc[warp][c][r * 8 + col + 1] = acc[c][1];
+  }
+  __syncthreads();
+  for (int vv = threadIdx.x; vv < kNeVals; vv += blockDim.x) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kNe2Warps; ++w) t += s_acc[w][vv / kGram][vv % kGram];
+    part[(int64_t)vv * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 // out[v] = sum_b part[v][b] in a fixed tree (one block per value).
 __global__ void __launch_bounds__(kBlock) k_reduce_cols(const double* __restrict__ part,
                                                         int nblocks, Ctl* __restrict__ ctl) {
@@ -139,11 +265,25 @@ __global__ void __launch_bounds__(kBlock) k_reduce_cols(const double* __restrict
   }
 }
 
-int launch_noise(fgbd_ctx* ctx, int64_t n, int patch) {
+int launch_noise(fgbd_ctx* ctx, int64_t n, int patch, int fuse_weights) {
   const int64_t nchunks = (n + 31) / 32;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, kNeGrid));
-  k_noise<<<grid, kNeThreads, 0, ctx->stream>>>(ctx->meta, ctx->ell, ctx->buf[BUF_Y], n, patch,
-                                                ctx->fslr, ctx->partials);
+  int grid;
+  if (ctx->ne_variant == 0) {
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, kNeGrid));
+    k_noise<<<grid, kNeThreads, 0, ctx->stream>>>(ctx->meta, ctx->nbr, ctx->buf[BUF_Y], n, patch,
+                                                  ctx->fslr, ctx->partials);
+  } else {
+    grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((nchunks + kNe2Warps - 1) / kNe2Warps, ctx->num_sms * 12));
+    if (fuse_weights)
+      k_noise2<true><<<grid, kNe2Warps * 32, 0, ctx->stream>>>(
+          ctx->meta, EllRef{ctx->nbr, ctx->pay}, (const double4*)ctx->buf[BUF_Y], n, patch, ctx->ctl, ctx->fslr,
+          ctx->partials);
+    else
+      k_noise2<false><<<grid, kNe2Warps * 32, 0, ctx->stream>>>(
+          ctx->meta, EllRef{ctx->nbr, ctx->pay}, (const double4*)ctx->buf[BUF_Y], n, patch, ctx->ctl, ctx->fslr,
+          ctx->partials);
+  }
   FGBD_LAUNCH(ctx);
   k_reduce_cols<<<kNeVals, kBlock, 0, ctx->stream>>>(ctx->partials, grid, ctx->ctl);
   FGBD_LAUNCH(ctx);

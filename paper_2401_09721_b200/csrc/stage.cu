@@ -20,7 +20,7 @@ __global__ void k_elig_flags(const uint32_t* __restrict__ meta, int64_t n, int D
     flag[i] = ((int)(meta[i] & 7u) >= D - 1) ? 1 : 0;
 }
 
-__global__ void k_extract(const uint32_t* __restrict__ meta, const int2* __restrict__ ell,
+__global__ void k_extract(const uint32_t* __restrict__ meta, const int* __restrict__ ell,
                           const double* __restrict__ colors, int64_t n, int D,
                           const int64_t* __restrict__ pos, int64_t ne,
                           int64_t* __restrict__ pidx, double* __restrict__ vec) {
@@ -34,7 +34,7 @@ __global__ void k_extract(const uint32_t* __restrict__ meta, const int2* __restr
     for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D] = colors[4 * i + c];
     for (int r = 1; r < D; ++r) {
       const int s = (int)((mt >> (3 + 3 * (r - 1))) & 7u);
-      const int64_t j = ell[eslot(s, n, i)].x;
+      const int64_t j = ell[eslot(s, n, i)];
       for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D + r] = colors[4 * j + c];
     }
   }
@@ -128,7 +128,7 @@ int32_t fgbd_extract_patches(fgbd_ctx* ctx, const double* colors, int32_t D,
         return fin(cuda_error(ctx, e, "alloc"));
       }
     }
-    k_extract<<<grid, kBlock, 0, ctx->stream>>>(ctx->meta, ctx->ell, ctx->buf[BUF_Y], n, D, pos,
+    k_extract<<<grid, kBlock, 0, ctx->stream>>>(ctx->meta, ctx->nbr, ctx->buf[BUF_Y], n, D, pos,
                                                 ne, d_pidx, d_vec);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
