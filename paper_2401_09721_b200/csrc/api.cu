@@ -351,6 +351,8 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_LF_VARIANT")) ctx->lf_variant = std::atoi(v);
   if (const char* v = std::getenv("FGBD_L2_PERSIST")) ctx->l2_persist = std::atoi(v);
   if (const char* v = std::getenv("FGBD_NE_VARIANT")) ctx->ne_variant = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_LF_SHAPE")) ctx->lf_shape = std::atoi(v) & 3;
+  if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (ensure_capacity(ctx, max_points > 0 ? max_points : 1, 0) != FGBD_OK) {
     set_error(nullptr, FGBD_E_CUDA, ctx->err);
     fgbd_ctx_destroy(ctx);

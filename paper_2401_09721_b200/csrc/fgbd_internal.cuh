@@ -33,6 +33,7 @@ namespace fgbd {
 
 constexpr int kBlock = 256;
 constexpr int kRedGrid = 148 * 4;      // fixed partition => deterministic sums
+constexpr int kRowsGrid = 148 * 8;     // k_rows partition (fixed => deterministic sigma_g)
 constexpr int kNeGrid = 148 * 16;      // NE blocks (96 threads: one warp per channel)
 constexpr int kSortThreads = 256;
 constexpr int kSortIPT = 16;
@@ -119,6 +120,8 @@ struct fgbd_ctx {
   unsigned int* tickets = nullptr;  // group tickets for hierarchical reductions
   int lf_variant = 10;          // filter-step kernel (FGBD_LF_VARIANT): 0 per-step, 2+ persistent
   int coop_blocks[64] = {};      // co-resident grid of each persistent instantiation
+  int lf_shape = 0;             // persistent kernel block shape (FGBD_LF_SHAPE)
+  int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)
   fgbd::Ctl* ctl = nullptr;     // device

@@ -366,8 +366,8 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
 // the same partials in the same order, so all reach the same decision.  A
 // stop decided at c discards the speculative x_{c+1}; q_max stops never
 // compute it.
-template <int WM, bool SELECT>
-__global__ void __launch_bounds__(kBlock, 3) k_lf_run(StepArgs a) {
+template <int WM, bool SELECT, int BLK = kBlock, int MINB = 3>
+__global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double s_red[32 * 3];
   __shared__ SelState s_st;
@@ -624,7 +624,7 @@ int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_ma
   a.mode = mode;
   a.early_exit = early_exit;
   a.sv2 = sigma_est * sigma_est;
-  k_mask<<<red_grid(n), kBlock, 0, ctx->stream>>>(a);
+  k_mask<<<fill_grid(ctx, n), kBlock, 0, ctx->stream>>>(a);
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
 }
@@ -643,21 +643,33 @@ static StepArgs step_args(fgbd_ctx* ctx, int64_t n) {
   return a;
 }
 
-template <int WM, bool SELECT>
-static int launch_run(fgbd_ctx* ctx, StepArgs& a) {
-  auto kern = k_lf_run<WM, SELECT>;
-  const int slot = WM * 2 + (SELECT ? 1 : 0);
+template <int WM, bool SELECT, int BLK, int MINB>
+static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
+  auto kern = k_lf_run<WM, SELECT, BLK, MINB>;
   if (ctx->coop_blocks[slot] == 0) {
     int per_sm = 0;
-    FGBD_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0));
+    FGBD_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLK, 0));
     ctx->coop_blocks[slot] = std::max(1, per_sm) * ctx->num_sms;
   }
   const int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>((a.n + kBlock - 1) / kBlock, ctx->coop_blocks[slot]));
+      1, std::min<int64_t>((a.n + BLK - 1) / BLK, ctx->coop_blocks[slot]));
   void* args[] = {&a};
-  FGBD_CUDA(ctx, cudaLaunchCooperativeKernel((void*)kern, grid, kBlock, args, 0, ctx->stream));
+  FGBD_CUDA(ctx, cudaLaunchCooperativeKernel((void*)kern, grid, BLK, args, 0, ctx->stream));
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
+}
+
+// block shape of the persistent kernel (FGBD_LF_SHAPE): 0 = 256 x 3/SM,
+// 1 = 256 x 4/SM (64 registers), 2 = 384 x 2/SM, 3 = 512 x 2/SM (64 registers)
+template <int WM, bool SELECT>
+static int launch_run(fgbd_ctx* ctx, StepArgs& a) {
+  const int base = (WM * 2 + (SELECT ? 1 : 0)) * 4 + ctx->lf_shape;
+  switch (ctx->lf_shape) {
+    case 1: return launch_run_k<WM, SELECT, 256, 4>(ctx, a, base);
+    case 2: return launch_run_k<WM, SELECT, 384, 2>(ctx, a, base);
+    case 3: return launch_run_k<WM, SELECT, 512, 2>(ctx, a, base);
+    default: return launch_run_k<WM, SELECT, 256, 3>(ctx, a, base);
+  }
 }
 
 // Weight source for the persistent kernels: variant 11 recomputes them from

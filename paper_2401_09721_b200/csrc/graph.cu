@@ -73,14 +73,20 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
         code = keys_in[i];
       }
     }
+    const unsigned vmask = __ballot_sync(kFull, valid);
     for (int l = 0; l < nlines; ++l) {
       const K key = FROM_COORDS ? line_key(code, l, b) : code;
       for (int p = 0; p < passes; ++p) {
         const unsigned d = valid ? (unsigned)((key >> (8 * p)) & 0xff) : 0x100u;
-        const unsigned peers = __match_any_sync(kFull, d);
-        const int leader = 31 - __clz(peers);
-        if (valid && lane == leader)
-          atomicAdd(&s_hist[(l * passes + p) * kRadix + d], (uint32_t)__popc(peers));
+        // a digit shared by the whole warp (raster-ordered input, high
+        // bytes) costs one atomic; otherwise per-lane atomics, which only
+        // contend when equal digits are scattered across the warp
+        const unsigned d0 = __shfl_sync(kFull, d, 0);
+        if (__all_sync(kFull, d == d0) && d0 < 0x100u) {
+          if (lane == 0) atomicAdd(&s_hist[(l * passes + p) * kRadix + d0], (uint32_t)__popc(vmask));
+        } else if (valid) {
+          atomicAdd(&s_hist[(l * passes + p) * kRadix + d], 1u);
+        }
       }
     }
   }
@@ -133,7 +139,7 @@ constexpr unsigned long long kFlagAgg = 1ull << 32;
 constexpr unsigned long long kFlagPre = 2ull << 32;
 
 template <typename K, bool FIRST, bool LAST, bool SLG>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(SortPass p) {
+__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(SortPass p) {
   extern __shared__ __align__(16) unsigned char smem[];
   K* s_keys = reinterpret_cast<K*>(smem);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kSortTile);
@@ -586,7 +592,7 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
   FGBD_CUDA(ctx, cudaMemsetAsync(S.tile_ctr, 0, kMaxPasses * 3 * sizeof(unsigned), ctx->stream));
   {
     const size_t smem = nh * sizeof(uint32_t);
-    const int grid = grid_for(n, ctx->num_sms * 2);
+    const int grid = grid_for(n, ctx->num_sms * ctx->prep_mult);
     if (SLG) {
       k_prep<K, true><<<grid, kBlock, smem, ctx->stream>>>(
           ctx->cur_coords, nullptr, n, b, nlines, passes, (K*)ctx->pc, S.hist, ctx->ctl);
@@ -640,7 +646,7 @@ static int graph_impl(fgbd_ctx* ctx, int64_t n, int b) {
                                                   ctx->cand);
     FGBD_LAUNCH(ctx);
   }
-  const int grid = grid_for(n, kRedGrid);
+  const int grid = grid_for(n, kRowsGrid);
   if (b > 15) {
     k_rows<K, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b,
                                                       EllRef{ctx->nbr, ctx->pay}, ctx->meta, ctx->partials,

@@ -154,7 +154,7 @@ __device__ __forceinline__ double patch_std(const double4 (&v)[7], int c, int D)
 }
 
 template <bool WEIGHTS>
-__global__ void __launch_bounds__(kNe2Warps * 32) k_noise2(const uint32_t* __restrict__ meta,
+__global__ void __launch_bounds__(kNe2Warps * 32, 6) k_noise2(const uint32_t* __restrict__ meta,
                                                            EllRef ell,
                                                            const double4* __restrict__ colors,
                                                            int64_t n, int D,

@@ -19,7 +19,7 @@ for d in data[(frames - 1) * n:]:
     k = d["Kernel Name"].split("(")[0][:58]
     v = float(d["Metric Value"].replace(",", ""))
     u = d["Metric Unit"]
-    v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+    v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(u, 1.0)
     a = agg.setdefault(k, [0, 0.0])
     a[0] += 1
     a[1] += v
