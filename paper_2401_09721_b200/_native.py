@@ -261,9 +261,15 @@ class PinnedPool:
             self.outstanding -= 1
 
 
-_pool = PinnedPool()
+_pool = PinnedPool(max_blocks=64)    # denoise outputs
+_user_pool = PinnedPool(max_blocks=1 << 20)  # explicit pinned_empty() requests
 
 
 def pinned_empty(shape, dtype) -> np.ndarray:
-    """numpy array backed by recycled page-locked host memory."""
+    """numpy array backed by recycled page-locked host memory (for inputs)."""
+    return _user_pool.empty(shape, dtype)
+
+
+def pinned_output(shape, dtype) -> np.ndarray:
+    """Output buffer for denoise results (bounded pool, recycled)."""
     return _pool.empty(shape, dtype)

@@ -2,6 +2,7 @@
 // (reference filtering.py:259-328) and the stage entry points.
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -271,6 +272,15 @@ int check_graph_ctl(fgbd_ctx* ctx, int bits) {
   return FGBD_OK;
 }
 
+// Contexts on one device run their kernel sections one at a time: the
+// persistent filter kernel needs the whole GPU, so interleaving two frames'
+// kernels only slows both.  Transfers stay outside the lock, so with several
+// host threads frame f+1's upload and frame f-1's download overlap frame f.
+std::mutex& device_mutex(int device) {
+  static std::mutex m[64];
+  return m[device & 63];
+}
+
 double ev_sec(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
@@ -430,6 +440,8 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   if ((rc = ensure_capacity(ctx, n, 3 * bits > 32))) return rc;
   apply_l2_policy(ctx, n);
   if (!dev && (rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false))) return rc;
+  if (!dev) FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  std::unique_lock<std::mutex> compute_lock(device_mutex(ctx->device));
   // the side stream starts after the coordinates have landed (full PCIe
   // bandwidth for them) and after all earlier main-stream work on the
   // staging buffers; it then overlaps the colour upload with the graph build
@@ -478,6 +490,9 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   }
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
+  FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->stream));
+  FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_side));
+  compute_lock.unlock();
   if (!dev && (rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), false))) return rc;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
   if ((rc = pull_ctl(ctx))) return rc;

@@ -275,7 +275,7 @@ def denoise(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
             raise NoiseEstimationError(f"unknown divisor rule {cfg.tau_divisor!r}")
         cfg = FilterConfig(**{**cfg.__dict__, "tau_divisor": "count"})
     ctx = nat.context()
-    out = nat.pinned_empty((n, 3), np.float64)  # full-rate D2H, recycled
+    out = nat.pinned_output((n, 3), np.float64)  # full-rate D2H, recycled
     rep = nat.Report()
     cq = -1 if cached_q is None else int(cached_q)
     cs = float("nan") if cached_sigma_est is None else float(cached_sigma_est)

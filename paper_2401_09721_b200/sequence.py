@@ -57,24 +57,35 @@ def plan_sequence(n_frames: int, interval: int, world: int = 1) -> tuple[list[li
     return phase1, phase2
 
 
+_executors: dict[int, ThreadPoolExecutor] = {}
+
+
 def _run_many(fn, items, workers):
+    """Map over persistent worker threads: each keeps its device context
+    (stream + scratch) across calls, so no per-sequence context setup."""
     if workers <= 1 or len(items) <= 1:
         return [fn(x) for x in items]
-    with ThreadPoolExecutor(max_workers=workers) as pool:
-        return list(pool.map(fn, items))
+    ex = _executors.get(workers)
+    if ex is None:
+        ex = _executors[workers] = ThreadPoolExecutor(max_workers=workers,
+                                                      thread_name_prefix="fgbd-worker")
+    return list(ex.map(fn, items))
 
 
 def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
                      cfg: FilterConfig = FilterConfig(), *, n_frames: int | None = None,
-                     workers: int = 2, process_group=None,
-                     denoise_fn=denoise) -> dict[int, tuple[PointCloud, DenoiseReport]]:
+                     workers: int = 2, process_group=None, denoise_fn=denoise,
+                     sink: Callable[[int, PointCloud, DenoiseReport], object] | None = None,
+                     ) -> dict[int, tuple[PointCloud, DenoiseReport]]:
     """Denoise a frame sequence with the reference's every-K-frames q reuse.
 
     `frames` is a sequence of PointClouds or a loader `i -> PointCloud`
     (frames are only materialised on the rank that processes them).  With a
     `torch.distributed` process group the work is split across its ranks and
     each rank returns the frames it processed; otherwise all frames are
-    returned.  `denoise_fn` defaults to the B200 `denoise`.
+    returned.  `denoise_fn` defaults to the B200 `denoise`.  With `sink`, each
+    finished frame is handed to `sink(index, cloud, report)` (e.g. a PLY
+    writer) and only the reports are kept, so output buffers recycle.
     """
     load = frames if callable(frames) else (lambda i: frames[i])
     n = n_frames if n_frames is not None else len(frames)  # type: ignore[arg-type]
@@ -86,8 +97,15 @@ def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
     phase1, phase2 = plan_sequence(n, cfg.reestimate_interval, world)
     results: dict[int, tuple[PointCloud, DenoiseReport]] = {}
 
+    def finish(f, res):
+        if sink is None:
+            return res
+        sink(f, res[0], res[1])
+        return (None, res[1])
+
     mine = phase1[rank]
-    for f, res in zip(mine, _run_many(lambda f: denoise_fn(load(f), cfg), mine, workers)):
+    for f, res in zip(mine, _run_many(lambda f: finish(f, denoise_fn(load(f), cfg)), mine,
+                                      workers)):
         results[f] = res
     cached = {f: (results[f][1].selected_q, results[f][1].sigma_est) for f in mine}
     if world > 1:
@@ -100,7 +118,7 @@ def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
 
     def run_cached(p: FramePlan):
         q, s = cached[p.head]
-        return denoise_fn(load(p.frame), cfg, cached_q=q, cached_sigma_est=s)
+        return finish(p.frame, denoise_fn(load(p.frame), cfg, cached_q=q, cached_sigma_est=s))
 
     todo = phase2[rank]
     for p, res in zip(todo, _run_many(run_cached, todo, workers)):
