@@ -240,6 +240,27 @@ int32_t fgbd_select_tail(const double* lam, int32_t d, int32_t tau_divisor,
                          int32_t* m, double* tau, int32_t* fallback,
                          char* err, int32_t err_len);
 
+/* ---- spatial slab partition of one frame over P ranks ---- */
+/* Every rank builds the whole graph; rank r filters rows [n*r/P, n*(r+1)/P)
+ * and reads foreign neighbours from the owner's buffers over peer memory.
+ * emulated != 0 runs all P ranks as block groups of one cooperative launch
+ * on this context's GPU (bit-identical protocol, used for testing);
+ * otherwise one process per GPU exchanges fgbd_slab_export handles (IPC)
+ * and calls fgbd_slab_import before the first fgbd_denoise_slab. */
+typedef struct fgbd_slab fgbd_slab;
+fgbd_slab* fgbd_slab_create(fgbd_ctx* ctx, int32_t world, int32_t rank, int64_t n,
+                            int32_t emulated);
+void fgbd_slab_destroy(fgbd_ctx* ctx, fgbd_slab* slab);
+int32_t fgbd_slab_handle_size(void);
+int32_t fgbd_slab_export(fgbd_ctx* ctx, fgbd_slab* slab, uint8_t* handle_out);
+int32_t fgbd_slab_import(fgbd_ctx* ctx, fgbd_slab* slab, const uint8_t* handles);
+/* denoise (filtering.py:259-328) with the filter loop split over the slab
+ * ranks; every rank returns the full frame. */
+int32_t fgbd_denoise_slab(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coords,
+                          const double* colors, int64_t n, int32_t bit_depth,
+                          const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
+                          double* out_colors, fgbd_report* report, uint32_t flags);
+
 /* pinned host buffers for zero-staging transfers */
 void* fgbd_host_alloc(int64_t bytes);
 void fgbd_host_free(void* p);

@@ -100,6 +100,13 @@ _SIGNATURES = {
     "fgbd_symmetric_eigenvalues": (c_i32, [C.c_void_p, c_i32, C.c_void_p, C.c_char_p, c_i32]),
     "fgbd_select_tail": (c_i32, [C.c_void_p, c_i32, c_i32, P(c_i32), P(c_f64), P(c_i32),
                                  C.c_char_p, c_i32]),
+    "fgbd_slab_create": (C.c_void_p, [C.c_void_p, c_i32, c_i32, c_i64, c_i32]),
+    "fgbd_slab_destroy": (None, [C.c_void_p, C.c_void_p]),
+    "fgbd_slab_handle_size": (c_i32, []),
+    "fgbd_slab_export": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "fgbd_slab_import": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "fgbd_denoise_slab": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_i32,
+                                  P(Config), c_i32, c_f64, C.c_void_p, P(Report), c_u32]),
     "fgbd_host_alloc": (C.c_void_p, [c_i64]),
     "fgbd_host_free": (None, [C.c_void_p]),
 }

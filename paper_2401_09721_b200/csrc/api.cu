@@ -410,9 +410,31 @@ void fgbd_host_free(void* p) {
   if (p) cudaFreeHost(p);
 }
 
+static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coords,
+                            const double* colors, int64_t n, int32_t bits,
+                            const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
+                            double* out_colors, fgbd_report* rep, uint32_t flags);
+
 int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors, int64_t n,
                      int32_t bits, const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
                      double* out_colors, fgbd_report* rep, uint32_t flags) {
+  return denoise_impl(ctx, nullptr, coords, colors, n, bits, cfg, cached_q, cached_sigma,
+                      out_colors, rep, flags);
+}
+
+int32_t fgbd_denoise_slab(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coords,
+                          const double* colors, int64_t n, int32_t bits, const fgbd_config* cfg,
+                          int32_t cached_q, double cached_sigma, double* out_colors,
+                          fgbd_report* rep, uint32_t flags) {
+  if (!slab) return set_error(ctx, FGBD_E_ARG, "null slab");
+  return denoise_impl(ctx, slab, coords, colors, n, bits, cfg, cached_q, cached_sigma,
+                      out_colors, rep, flags);
+}
+
+static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coords,
+                            const double* colors, int64_t n, int32_t bits,
+                            const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
+                            double* out_colors, fgbd_report* rep, uint32_t flags) {
   if (!ctx || !rep) return set_error(ctx, FGBD_E_ARG, "null context or report");
   cudaSetDevice(ctx->device);
   ctx->err.clear();
@@ -461,9 +483,14 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   if (cached_q >= 0) {
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
     int fin = BUF_Y;
-    if ((rc = launch_fixed_steps(ctx, n, cached_q, w64, &fin))) return rc;
-    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
-    if ((rc = launch_compact(ctx, n, fin, dev ? out_colors : ctx->out, 1))) return rc;
+    if (slab) {
+      if ((rc = launch_slab(ctx, slab, n, 0, cached_q, dev ? out_colors : ctx->out))) return rc;
+      if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
+    } else {
+      if ((rc = launch_fixed_steps(ctx, n, cached_q, w64, &fin))) return rc;
+      if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
+      if ((rc = launch_compact(ctx, n, fin, dev ? out_colors : ctx->out, 1))) return rc;
+    }
   } else {
     const int D = cfg->patch_size;
     if ((rc = launch_noise(ctx, n, D, fuse_w ? 1 : 0))) return rc;
@@ -485,9 +512,14 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
                           nullptr)))
       return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
-    if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) return rc;
-    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
-    if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
+    if (slab) {
+      if ((rc = launch_slab(ctx, slab, n, 1, 0, dev ? out_colors : ctx->out))) return rc;
+      if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
+    } else {
+      if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) return rc;
+      if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
+      if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
+    }
   }
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
   FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->stream));
@@ -497,6 +529,8 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
   if ((rc = pull_ctl(ctx))) return rc;
   if ((rc = check_graph_ctl(ctx, bits))) return rc;
+  if (ctx->ctl_host->err_flags & 4)
+    return set_error(ctx, FGBD_E_NCCL, "slab peer did not reach the barrier (timeout)");
   const Ctl& h = *ctx->ctl_host;
   rep->n_edges = (int64_t)h.n_edges;
   rep->nnz = 2 * (int64_t)h.n_edges;

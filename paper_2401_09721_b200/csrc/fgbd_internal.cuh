@@ -221,3 +221,9 @@ int launch_criterion(fgbd_ctx* ctx, const double* d_y, const double* d_x,
                      double* crit_out);
 
 }  // namespace fgbd
+
+struct fgbd_slab;
+namespace fgbd {
+int launch_slab(fgbd_ctx* ctx, fgbd_slab* s, int64_t n, int select, int fixed_steps,
+                double* d_out);
+}  // namespace fgbd

@@ -286,3 +286,38 @@ def test_sequence_driver_matches_reference_loop(gpu_ready):
                            cached_q=ref.selected_q, cached_sigma_est=ref.sigma_est)
             assert got[f][1].cached and got[f][1].selected_q == ref.selected_q
             assert np.max(np.abs(got[f][0].colors - rf.colors)) <= COLOR_ATOL
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 3, 4])
+@pytest.mark.parametrize("name", ["m20k_ramp_s10", "m20k_two-tone_s20", "l100k_constant_s10",
+                                  "c20k_ramp_s10_cached7", "v20k_two-tone_s20_per_channel"])
+def test_slab_partition_bit_identical(gpu_ready, name, ranks):
+    """P slab ranks (block groups of one cooperative
+    launch, peer-memory halo + flag barrier protocol) reproduce the
+    single-GPU colours bit for bit and the same q and S."""
+    from paper_2401_09721_b200.slab import denoise_slab
+
+    rec, arr, clean, pc = _input(name)
+    cfg = _cfg(rec)
+    kw = dict(cached_q=rec.get("cached_q"), cached_sigma_est=rec.get("cached_sigma"))
+    a, ra = fb.denoise(pc, cfg, **kw)
+    b, rb = denoise_slab(pc, cfg, emulate_ranks=ranks, **kw)
+    assert rb.selected_q == ra.selected_q == rec["report"]["selected_q"]
+    assert rb.device["steps"] == ra.device["steps"]
+    assert np.array_equal(a.colors, b.colors)
+    if not rb.cached:
+        np.testing.assert_allclose(rb.device["trace"], ra.device["trace"], rtol=CRIT_RTOL,
+                                   atol=CRIT_ATOL)
+
+
+@pytest.mark.slow
+def test_slab_partition_full_size(gpu_ready):
+    from paper_2401_09721_b200.slab import denoise_slab
+
+    rec, arr, clean, pc = _input("x1m_ramp_s10")
+    a, ra = fb.denoise(pc)
+    for ranks in (2, 8):
+        b, rb = denoise_slab(pc, emulate_ranks=ranks)
+        assert rb.selected_q == ra.selected_q == rec["report"]["selected_q"]
+        assert rb.device["steps"] == rec["steps"]
+        assert np.array_equal(a.colors, b.colors)

@@ -109,3 +109,39 @@ def test_two_rank_gloo_matches_single_process():
         assert q == ref[f][1].selected_q and cached == ref[f][1].cached
         assert sigma == ref[f][1].sigma_est
         assert np.array_equal(colors, ref[f][0].colors)
+
+
+def _handle_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+
+    from paper_2401_09721_b200.slab import exchange_handles, slab_bounds
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    got = exchange_handles(bytes([rank]) * 64, dist.group.WORLD)
+    with open(os.path.join(outdir, f"h{rank}.pkl"), "wb") as fh:
+        pickle.dump((got, slab_bounds(1_000_003, world)), fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_slab_handle_exchange_gloo():
+    """The slab mode's one host-side collective: every rank gets every rank's
+    IPC handle in rank order, and all ranks agree on the row ranges."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_handle_worker, args=(2, _free_port(), d), nprocs=2, join=True,
+                           start_method="spawn")
+        res = [pickle.load(open(os.path.join(d, f"h{r}.pkl"), "rb")) for r in range(2)]
+    for got, bounds in res:
+        assert got == [bytes([0]) * 64, bytes([1]) * 64]
+        assert bounds == res[0][1] and bounds[0] == 0 and bounds[-1] == 1_000_003
+
+
+@pytest.mark.parametrize("n,world", [(10, 3), (1_000_000, 8), (7, 7), (8_000_000, 5)])
+def test_slab_bounds_partition(n, world):
+    from paper_2401_09721_b200.slab import slab_bounds
+
+    b = slab_bounds(n, world)
+    assert b[0] == 0 and b[-1] == n and all(b[i] <= b[i + 1] for i in range(world))
+    sizes = np.diff(b)
+    assert sizes.max() - sizes.min() <= 1
