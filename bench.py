@@ -56,8 +56,9 @@ def parse():
     ap.add_argument("--sigma", type=float, default=SIGMA)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="frame", choices=["frame", "video"],
-                    help="frame: BASELINE configs[1] (default); video: configs[3]")
+    ap.add_argument("--workload", default="frame", choices=["frame", "video", "slab"],
+                    help="frame: BASELINE configs[1] (default); video: configs[3]; "
+                         "slab: configs[4] (one frame split over the GPUs)")
     ap.add_argument("--frames", type=int, default=300, help="video length (configs[3])")
     ap.add_argument("--workers", type=int, default=2, help="host threads per GPU (video)")
     return ap.parse_args()
@@ -465,12 +466,87 @@ def run_video(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# slab workload (BASELINE.json configs[4]): one big frame over N GPUs
+# ---------------------------------------------------------------------------
+
+def run_slab(args):
+    import torch
+
+    import paper_2401_09721_b200 as fb
+    from paper_2401_09721_b200 import _native as nat
+    from paper_2401_09721_b200.slab import denoise_slab
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    fb.use_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist.group.WORLD
+    n = args.n if args.n != N_POINTS else 8_000_000
+    clean, _ = fb.generate_cloud(args.kind, n, seed=0)
+    noisy = fb.add_gaussian_noise(clean, args.sigma, seed=1)
+    c = nat.pinned_empty(noisy.coords.shape, np.int64)
+    c[...] = noisy.coords
+    y = nat.pinned_empty(noisy.colors.shape, np.float64)
+    y[...] = noisy.colors
+    pc = fb.PointCloud(c, y, noisy.bit_depth)
+    emulate = None if world > 1 else 1
+
+    def step():
+        if pg is not None:
+            return denoise_slab(pc, process_group=pg)
+        return denoise_slab(pc, emulate_ranks=1)
+
+    for _ in range(max(args.warmup, 3)):
+        out, rep = step()
+    walls, devs = [], []
+    for _ in range(args.steps):
+        if pg is not None:
+            import torch.distributed as dist
+
+            dist.barrier()
+        t0 = time.perf_counter()
+        out, rep = step()
+        walls.append(time.perf_counter() - t0)
+        devs.append(rep.device["t_total"])
+    wall = float(np.sum(walls))
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([wall], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": f"frames/sec, one {n:,}-point frame slab-partitioned over the GPUs",
+            "value": args.steps / wall, "unit": "frames/s", "n_gpus": world,
+            "ms_per_step": 1e3 * wall / args.steps, "steps": args.steps,
+            "higher_is_better": True, "scaling": "strong", "dtype": "f64", "data": "synthetic",
+            "device_ms_rank0": 1e3 * float(np.mean(devs)),
+            "stage_ms": {k: 1e3 * v for k, v in rep.stage_timings.items()},
+            "config": {"workload": "BASELINE.json configs[4]", "kind": args.kind, "n_points": n,
+                       "sigma": args.sigma, "selected_q": rep.selected_q,
+                       "filter_steps_S": rep.device["steps"], "slab_ranks": world,
+                       "emulated": emulate is not None},
+        }), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "video":
         run_video(args)
+    elif args.workload == "slab":
+        run_slab(args)
     else:
         run_b200(args)
 
