@@ -261,6 +261,27 @@ int32_t fgbd_denoise_slab(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coords,
                           const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
                           double* out_colors, fgbd_report* report, uint32_t flags);
 
+/* ---- PLY binary vertex records (ply.py:134-287) ---- */
+/* type codes: 0 int8, 1 uint8, 2 int16, 3 uint16, 4 int32, 5 uint32,
+ * 6 float32, 7 float64.  offsets/types: x, y, z, red, green, blue. */
+/* decode packed little-endian records into coords (int64 when coords_int is
+ * given, else float64) and colours float64; *bit_length receives the bit
+ * length of the largest integer coordinate (infer_bit_depth). */
+int32_t fgbd_ply_decode(fgbd_ctx* ctx, const uint8_t* body, int64_t n, int32_t stride,
+                        const int32_t* offsets, const int32_t* types, int64_t* coords_int,
+                        double* coords_float, double* colors, int32_t* bit_length,
+                        uint32_t flags);
+/* encode 15-byte records (uint32 or float32 x/y/z, colours rounded half-up
+ * to uint8), byte-identical to the reference save_ply body. */
+int32_t fgbd_ply_encode(fgbd_ctx* ctx, const int64_t* coords_int, const double* coords_float,
+                        const double* colors, int64_t n, uint8_t* body_out, uint32_t flags);
+/* decode -> denoise -> encode on the device: raw vertex records in, the
+ * denoised frame's records (save_ply layout) out.  bit_depth <= 0 infers it. */
+int32_t fgbd_denoise_ply(fgbd_ctx* ctx, const uint8_t* body, int64_t n, int32_t stride,
+                         const int32_t* offsets, const int32_t* types, int32_t bit_depth,
+                         const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
+                         uint8_t* body_out, fgbd_report* report, uint32_t flags);
+
 /* pinned host buffers for zero-staging transfers */
 void* fgbd_host_alloc(int64_t bytes);
 void fgbd_host_free(void* p);

@@ -107,6 +107,12 @@ _SIGNATURES = {
     "fgbd_slab_import": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "fgbd_denoise_slab": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_i32,
                                   P(Config), c_i32, c_f64, C.c_void_p, P(Report), c_u32]),
+    "fgbd_ply_decode": (c_i32, [C.c_void_p, C.c_void_p, c_i64, c_i32, P(c_i32), P(c_i32),
+                                C.c_void_p, C.c_void_p, C.c_void_p, P(c_i32), c_u32]),
+    "fgbd_ply_encode": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, c_i64,
+                                C.c_void_p, c_u32]),
+    "fgbd_denoise_ply": (c_i32, [C.c_void_p, C.c_void_p, c_i64, c_i32, P(c_i32), P(c_i32), c_i32,
+                                 P(Config), c_i32, c_f64, C.c_void_p, P(Report), c_u32]),
     "fgbd_host_alloc": (C.c_void_p, [c_i64]),
     "fgbd_host_free": (None, [C.c_void_p]),
 }
@@ -228,12 +234,16 @@ class PinnedPool:
     `denoise` returns its colours in one of these blocks so the D2H copy runs
     at full PCIe rate; the block goes back to the pool when the returned
     array (and every view of it) is garbage-collected.  Past `max_blocks`
-    outstanding blocks it falls back to ordinary pageable memory.
+    outstanding blocks it falls back to ordinary pageable memory.  Block
+    sizes are rounded up to 8 classes per octave (<= 12.5% slack) so frames
+    of varying size share blocks, and at most `max_free_bytes` are kept idle.
     """
 
-    def __init__(self, max_blocks: int = 16):
+    def __init__(self, max_blocks: int = 16, max_free_bytes: int = 8 << 30):
         self.max_blocks = max_blocks
+        self.max_free_bytes = max_free_bytes
         self.free: dict[int, list[int]] = {}
+        self.free_bytes = 0
         self.outstanding = 0
         self.allocs = 0
         self.reuses = 0
@@ -242,10 +252,12 @@ class PinnedPool:
     def empty(self, shape, dtype) -> np.ndarray:
         dtype = np.dtype(dtype)
         count = int(np.prod(shape))
-        size = max(count * dtype.itemsize, 1)
+        size = size_class(max(count * dtype.itemsize, 1))
         with self.lock:
             lst = self.free.get(size)
             ptr = lst.pop() if lst else None
+            if ptr is not None:
+                self.free_bytes -= size
             if ptr is None and self.outstanding >= self.max_blocks:
                 return np.empty(shape, dtype)
             self.outstanding += 1
@@ -264,8 +276,20 @@ class PinnedPool:
 
     def _release(self, size, ptr):
         with self.lock:
-            self.free.setdefault(size, []).append(ptr)
             self.outstanding -= 1
+            if self.free_bytes + size <= self.max_free_bytes:
+                self.free.setdefault(size, []).append(ptr)
+                self.free_bytes += size
+                return
+        load_library().fgbd_host_free(ptr)
+
+
+def size_class(size: int) -> int:
+    """Round up to one of 8 sizes per power of two (4 KiB minimum)."""
+    if size <= 4096:
+        return 4096
+    step = 1 << max(0, size.bit_length() - 4)
+    return (size + step - 1) // step * step
 
 
 _pool = PinnedPool(max_blocks=64)    # denoise outputs

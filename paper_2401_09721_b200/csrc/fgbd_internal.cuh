@@ -130,6 +130,8 @@ struct fgbd_ctx {
   int64_t* scan_tmp = nullptr;
   int64_t scan_cap = 0;
   void* csr_scratch = nullptr;
+  void* ply_stage = nullptr;     // PLY records in/out (fgbd_denoise_ply)
+  size_t ply_stage_bytes = 0;
   size_t csr_scratch_bytes = 0;
 
   cudaEvent_t ev[8] = {};

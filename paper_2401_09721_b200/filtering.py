@@ -267,13 +267,7 @@ def denoise(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
             stage_timings={"graph_construction": 0.0, "noise_estimation": 0.0,
                            "low_pass_filter": 0.0})
     bits = _require_quantized(pc_noisy)
-    if cached_q is not None and cached_q < 0:
-        raise FilterError(f"cached_q must be >= 0, got {cached_q}")
-    if cfg.tau_divisor not in ("count", "count_plus_one"):
-        from .errors import NoiseEstimationError
-        if cached_q is None:
-            raise NoiseEstimationError(f"unknown divisor rule {cfg.tau_divisor!r}")
-        cfg = FilterConfig(**{**cfg.__dict__, "tau_divisor": "count"})
+    cfg = _check_call(cfg, cached_q)
     ctx = nat.context()
     out = nat.pinned_output((n, 3), np.float64)  # full-rate D2H, recycled
     rep = nat.Report()
@@ -283,6 +277,26 @@ def denoise(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
                                    n, bits, nat.make_config(cfg), cq, cs, nat.ptr(out), rep, 0),
               "denoise")
     ctx.graph_token = None
+    report = _report_from(rep, cfg, cached_q, cached_sigma_est)
+    out.flags.writeable = False
+    return PointCloud._trusted(pc_noisy.coords, out, pc_noisy.bit_depth), report
+
+
+def _check_call(cfg: FilterConfig, cached_q) -> FilterConfig:
+    """Argument errors denoise raises (filtering.py:315, noise.py:205); an
+    unknown divisor rule only matters when noise is estimated."""
+    if cached_q is not None and cached_q < 0:
+        raise FilterError(f"cached_q must be >= 0, got {cached_q}")
+    if cfg.tau_divisor not in ("count", "count_plus_one"):
+        from .errors import NoiseEstimationError
+        if cached_q is None:
+            raise NoiseEstimationError(f"unknown divisor rule {cfg.tau_divisor!r}")
+        cfg = FilterConfig(**{**cfg.__dict__, "tau_divisor": "count"})
+    return cfg
+
+
+def _report_from(rep, cfg: FilterConfig, cached_q, cached_sigma_est) -> DenoiseReport:
+    """DenoiseReport of one device frame (filtering.py:300-328 field rules)."""
     timings = {"graph_construction": float(rep.t_graph_construction),
                "noise_estimation": float(rep.t_noise_estimation),
                "low_pass_filter": float(rep.t_low_pass_filter)}
@@ -290,15 +304,12 @@ def denoise(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
     if cached_q is None:
         if rep.all_excluded_fallback:
             warnings.warn("variance mask excluded every point; selecting unmasked")
-        report = DenoiseReport(
+        return DenoiseReport(
             selected_q=int(rep.selected_q), sigma_est=float(rep.sigma_est),
             masked_fraction=float(rep.masked_fraction), stage_timings=timings,
             criterion_value=float(rep.criterion_value), converged=bool(rep.converged),
             eligible_count=int(rep.eligible_count), device=info)
-    else:
-        report = DenoiseReport(
-            selected_q=int(cached_q),
-            sigma_est=float(cached_sigma_est) if cached_sigma_est is not None else 0.0,
-            masked_fraction=0.0, stage_timings=timings, cached=True, device=info)
-    out.flags.writeable = False
-    return PointCloud._trusted(pc_noisy.coords, out, pc_noisy.bit_depth), report
+    return DenoiseReport(
+        selected_q=int(cached_q),
+        sigma_est=float(cached_sigma_est) if cached_sigma_est is not None else 0.0,
+        masked_fraction=0.0, stage_timings=timings, cached=True, device=info)
