@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--sigma", type=float, default=SIGMA)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="frame", choices=["frame", "video", "slab"],
+    ap.add_argument("--workload", default="frame", choices=["frame", "video", "slab", "ply"],
                     help="frame: BASELINE configs[1] (default); video: configs[3]; "
                          "slab: configs[4] (one frame split over the GPUs)")
     ap.add_argument("--frames", type=int, default=300, help="video length (configs[3])")
@@ -426,8 +426,11 @@ def run_video(args):
     load = lambda i: pool[i % len(pool)]
     checksum = [0.0]
 
+    compute = []
+
     def sink(i, pc, rep):  # consume the frame (as a writer would) and release it
         checksum[0] += float(pc.colors[i % pc.n_points, 0])
+        compute.append(sum(rep.stage_timings.values()))
 
     # warm-up: contexts for every worker thread, pinned output pool
     denoise_sequence(load, cfg, n_frames=min(2 * cfg.reestimate_interval, args.frames),
@@ -437,6 +440,7 @@ def run_video(args):
 
         dist.barrier()
     torch.cuda.synchronize()
+    compute.clear()
     t0 = time.perf_counter()
     res = denoise_sequence(load, cfg, n_frames=args.frames, workers=args.workers,
                            process_group=pg, sink=sink)
@@ -456,7 +460,90 @@ def run_video(args):
             "value": args.frames / wall, "unit": "frames/s", "n_gpus": world,
             "wall_s": wall, "higher_is_better": True, "scaling": "strong", "dtype": "f64",
             "data": "synthetic", "workers_per_gpu": args.workers,
+            "device_compute_ms_sum_per_frame": 1e3 * float(np.sum(compute)) / args.frames,
             "config": {"workload": "BASELINE.json configs[3]", "kind": args.kind,
+                       "n_points": args.n, "sigma": args.sigma, "frames": args.frames,
+                       "rank0_heads": heads, "rank0_frames": len(res)},
+        }), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# ply workload: the CLI's directory-of-PLY-frames loop,
+# PLY file bytes in -> denoised PLY file bytes out, K-frame q reuse
+# ---------------------------------------------------------------------------
+
+def run_ply(args):
+    import torch
+
+    import paper_2401_09721_b200 as fb
+    from paper_2401_09721_b200 import _native as nat
+    from paper_2401_09721_b200.ply import denoise_ply, save_ply
+    from paper_2401_09721_b200.sequence import denoise_sequence
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    fb.use_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist.group.WORLD
+    # distinct noisy frames serialised as binary PLY files held in pinned memory
+    clean, _ = fb.generate_cloud(args.kind, args.n, seed=0)
+    files = []
+    for s in range(8):
+        b = save_ply(fb.add_gaussian_noise(clean, args.sigma, seed=1 + s))
+        f = nat.pinned_empty((len(b),), np.uint8)
+        f[...] = np.frombuffer(b, np.uint8)
+        files.append(f)
+    cfg = fb.FilterConfig()
+    load = lambda i: files[i % len(files)]
+    fn = lambda src, cfg, cached_q=None, cached_sigma_est=None: denoise_ply(
+        src, cfg, cached_q, cached_sigma_est, copy=False)
+    checksum = [0]
+
+    compute = []
+
+    def sink(i, out, rep):  # consume the output file bytes and release them
+        checksum[0] += int(out[-1])
+        compute.append(sum(rep.stage_timings.values()))
+
+    denoise_sequence(load, cfg, n_frames=min(2 * cfg.reestimate_interval, args.frames),
+                     workers=args.workers, process_group=pg, denoise_fn=fn, sink=sink)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    compute.clear()
+    t0 = time.perf_counter()
+    res = denoise_sequence(load, cfg, n_frames=args.frames, workers=args.workers,
+                           process_group=pg, denoise_fn=fn, sink=sink)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([wall], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+    if rank == 0:
+        heads = sum(1 for r in res.values() if not r[1].cached)
+        print(json.dumps({
+            "metric": f"frames/sec, {args.frames}-frame PLY sequence at {args.n:,} pts/frame "
+                      f"(binary PLY bytes in -> PLY bytes out, K={cfg.reestimate_interval})",
+            "value": args.frames / wall, "unit": "frames/s", "n_gpus": world,
+            "wall_s": wall, "higher_is_better": True, "scaling": "strong", "dtype": "f64",
+            "data": "synthetic", "workers_per_gpu": args.workers,
+            "device_compute_ms_sum_per_frame": 1e3 * float(np.sum(compute)) / args.frames,
+            "e2e": {"h2d_bytes_per_step": int(files[0].size),
+                    "d2h_bytes_per_step": int(files[0].size)},
+            "config": {"workload": "SURVEY 8(f) rank 2: PLY frame sequence", "kind": args.kind,
                        "n_points": args.n, "sigma": args.sigma, "frames": args.frames,
                        "rank0_heads": heads, "rank0_frames": len(res)},
         }), flush=True)
@@ -547,6 +634,8 @@ def main():
         run_video(args)
     elif args.workload == "slab":
         run_slab(args)
+    elif args.workload == "ply":
+        run_ply(args)
     else:
         run_b200(args)
 

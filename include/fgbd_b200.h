@@ -282,6 +282,19 @@ int32_t fgbd_denoise_ply(fgbd_ctx* ctx, const uint8_t* body, int64_t n, int32_t 
                          const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
                          uint8_t* body_out, fgbd_report* report, uint32_t flags);
 
+/* ---- brute-force kNN graph (graph.py:254-298) ------ */
+/* build_knn_brute: exact k nearest neighbours (ties by index), symmetrised by
+ * union (_graph_from_pairs, graph.py:179-208).  Coordinates are int64
+ * (coords_int, bit_depth known) or float64 (coords_float).  The graph stays
+ * in the context; *n_edges receives E. */
+int32_t fgbd_knn_build(fgbd_ctx* ctx, const int64_t* coords_int, const double* coords_float,
+                       int64_t n, int32_t k, int32_t bit_depth, int64_t* n_edges,
+                       uint32_t flags);
+/* Copy the held kNN graph out in the reference's Graph conventions: indptr
+ * (n+1), indices/csr_edge (2E), edge_u/edge_v/edge_sqdist (E). */
+int32_t fgbd_knn_export(fgbd_ctx* ctx, int64_t* indptr, int64_t* indices, int64_t* csr_edge,
+                        int64_t* edge_u, int64_t* edge_v, double* edge_sqdist);
+
 /* pinned host buffers for zero-staging transfers */
 void* fgbd_host_alloc(int64_t bytes);
 void fgbd_host_free(void* p);

@@ -199,6 +199,65 @@ def build_weighted_slg(coords, bit_depth) -> OracleGraph:
     return apply_gaussian_weights(g, compute_sigma_g(g))
 
 
+def knn_rows(coords: np.ndarray, k: int, queries=None, chunk: int = 256) -> np.ndarray:
+    """Exact k nearest neighbours (graph.py:254-285) for the given query rows.
+
+    The reference scans j ascending and inserts on a strict `<`, so its row
+    is the k smallest (squared distance, index) pairs, j != i.  Restated as a
+    lexicographic selection over fp64 distances ((dx*dx + dy*dy) + dz*dz).
+    """
+    g = np.asarray(coords, np.float64)
+    n = g.shape[0]
+    if not 1 <= k < n:
+        raise OracleError("graph", f"k must satisfy 1 <= k < n_points, got k={k}, n={n}")
+    q = np.arange(n) if queries is None else np.asarray(queries, np.int64)
+    out = np.empty((q.size, k), np.int64)
+    idx = np.arange(n)
+    for s0 in range(0, q.size, chunk):
+        qs = q[s0:s0 + chunk]
+        d = g[None, :, :] - g[qs, None, :]
+        d2 = (d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1]) + d[..., 2] * d[..., 2]
+        d2[np.arange(qs.size), qs] = np.inf  # never its own neighbour
+        for r in range(qs.size):
+            order = np.lexsort((idx, d2[r]))
+            out[s0 + r] = order[:k]
+    return out
+
+
+def graph_from_pairs(coords: np.ndarray, u: np.ndarray, v: np.ndarray) -> OracleGraph:
+    """Undirected union of directed pairs (graph.py:179-208) as an OracleGraph:
+    rows are the sorted distinct partners of each vertex; edges the upper
+    triangle row-major (== np.unique of lo * n + hi)."""
+    g = np.asarray(coords)
+    n = g.shape[0]
+    u = np.asarray(u, np.int64)
+    v = np.asarray(v, np.int64)
+    keep = u != v
+    src = np.concatenate([u[keep], v[keep]])
+    dst = np.concatenate([v[keep], u[keep]])
+    key = np.unique(src * n + dst)
+    row, indices = key // n, key % n
+    indptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(row, minlength=n), out=indptr[1:])
+    upper = indices > row
+    edge_u, edge_v = row[upper], indices[upper]
+    ukey = edge_u * n + edge_v
+    skey = np.where(upper, row * n + indices, indices * n + row)
+    csr_edge = np.searchsorted(ukey, skey).astype(np.int64)
+    d = g[edge_u].astype(np.float64) - g[edge_v].astype(np.float64)
+    # np.einsum("ij,ij->i") over 3 terms adds as (x*x + z*z) + y*y (its
+    # two-lane inner loop); exact for integer coordinates, visible for floats
+    sqdist = (d[:, 0] * d[:, 0] + d[:, 2] * d[:, 2]) + d[:, 1] * d[:, 1]
+    return OracleGraph(n, indptr, indices.astype(np.int64), csr_edge, edge_u, edge_v, sqdist)
+
+
+def build_knn_brute(coords: np.ndarray, k: int) -> OracleGraph:
+    """graph.py:288-298 restated: knn_rows + graph_from_pairs."""
+    nb = knn_rows(coords, k)
+    n = nb.shape[0]
+    return graph_from_pairs(coords, np.repeat(np.arange(n), k), nb.reshape(-1))
+
+
 # --------------------------------------------------------------------------
 # a9-a13: NE-GBP
 # --------------------------------------------------------------------------

@@ -113,6 +113,9 @@ _SIGNATURES = {
                                 C.c_void_p, c_u32]),
     "fgbd_denoise_ply": (c_i32, [C.c_void_p, C.c_void_p, c_i64, c_i32, P(c_i32), P(c_i32), c_i32,
                                  P(Config), c_i32, c_f64, C.c_void_p, P(Report), c_u32]),
+    "fgbd_knn_build": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_i32, c_i32,
+                               P(c_i64), c_u32]),
+    "fgbd_knn_export": (c_i32, [C.c_void_p] + [C.c_void_p] * 6),
     "fgbd_host_alloc": (C.c_void_p, [c_i64]),
     "fgbd_host_free": (None, [C.c_void_p]),
 }

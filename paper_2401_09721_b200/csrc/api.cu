@@ -385,6 +385,7 @@ void fgbd_ctx_destroy(fgbd_ctx* ctx) {
   if (ctx->tickets) cudaFree(ctx->tickets);
   if (ctx->csr_scratch) cudaFree(ctx->csr_scratch);
   if (ctx->ply_stage) cudaFree(ctx->ply_stage);
+  if (ctx->aux) cudaFree(ctx->aux);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->side) cudaStreamSynchronize(ctx->side);

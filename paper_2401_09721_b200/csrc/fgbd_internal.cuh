@@ -132,6 +132,10 @@ struct fgbd_ctx {
   void* csr_scratch = nullptr;
   void* ply_stage = nullptr;     // PLY records in/out (fgbd_denoise_ply)
   size_t ply_stage_bytes = 0;
+  void* aux = nullptr;           // off-path scratch (kNN graph), grown on demand
+  size_t aux_bytes = 0;
+  int64_t knn_n = -1, knn_e = 0;  // kNN graph held in aux
+  size_t knn_off[6] = {0, 0, 0, 0, 0, 0};
   size_t csr_scratch_bytes = 0;
 
   cudaEvent_t ev[8] = {};

@@ -59,6 +59,7 @@ class Graph:
     edge_weights: np.ndarray | None = None
     _token: int = 0
     _bits: int = 0
+    _slg: bool = False  # built here as the scan-line graph of its cloud
 
     def __post_init__(self):
         for name in ("indptr", "indices", "csr_edge", "edge_u", "edge_v"):
@@ -175,7 +176,8 @@ def _export(ctx, info, weighted: bool, bits: int) -> Graph:
     tok = next(_tokens)
     ctx.graph_token = tok
     sg = float(info.sigma_g) if weighted else None
-    return Graph(n, indptr, indices, csr_edge, eu, ev, sq, sg, w, _token=tok, _bits=bits)
+    return Graph(n, indptr, indices, csr_edge, eu, ev, sq, sg, w, _token=tok, _bits=bits,
+                 _slg=True)
 
 
 def build_slg(pc: PointCloud) -> Graph:
@@ -216,7 +218,7 @@ def apply_gaussian_weights(g: Graph, sigma_g: float) -> Graph:
                                             float(sigma_g), None, nat.ptr(w), 0),
                   "apply_gaussian_weights")
     return Graph(g.n, g.indptr, g.indices, g.csr_edge, g.edge_u, g.edge_v, g.edge_sqdist,
-                 float(sigma_g), w, _token=g._token, _bits=g._bits)
+                 float(sigma_g), w, _token=g._token, _bits=g._bits, _slg=g._slg)
 
 
 def ensure_device_graph(pc: PointCloud, g: Graph | None, weights64: bool = False):
@@ -224,7 +226,11 @@ def ensure_device_graph(pc: PointCloud, g: Graph | None, weights64: bool = False
 
     Reuses the held copy when `g` is the graph this context built last;
     otherwise rebuilds it on the device from the cloud (the SLG is a pure
-    function of the coordinates).
+    function of the coordinates).  The device noise estimator and q scan run
+    on the scan-line graph only: a graph built elsewhere (by hand, from
+    fixtures) is accepted when it IS that graph -- same edges, and weights
+    at its sigma_g equal to the device's -- and rejected loudly otherwise
+    (`apply_filter` / `filter_step` take any CSR graph).
     """
     ctx = nat.context()
     if g is not None and g._token and ctx.graph_token == g._token and not weights64:
@@ -232,11 +238,53 @@ def ensure_device_graph(pc: PointCloud, g: Graph | None, weights64: bool = False
     if g is not None and g.n != pc.n_points:
         raise GraphError(f"graph has {g.n} vertices for a {pc.n_points}-point cloud")
     ctx, info = _device_build(pc, weights64)
+    if g is not None and not g._slg:
+        _check_is_slg(ctx, info, g)
     ctx.graph_token = g._token if g is not None and g._token else None
     return ctx
 
 
-def build_knn_brute(pc: PointCloud, k: int) -> Graph:  # pragma: no cover - out of scope
-    """Brute-force kNN (graph.py:254-298) is a bench-graph baseline, not on the
-    denoise path; it is not provided by the B200 build."""
-    raise NotImplementedError("build_knn_brute is outside the B200 hot path (SURVEY 8(f) rank 4)")
+def _check_is_slg(ctx, info, g: Graph) -> None:
+    same = int(info.n_edges) == g.n_edges
+    if same and g.n_edges:
+        eu = np.empty(g.n_edges, np.int64)
+        ev = np.empty(g.n_edges, np.int64)
+        w = np.empty(g.n_edges, np.float64) if g.is_weighted else None
+        ctx.check(ctx.lib.fgbd_graph_export(ctx.handle, None, None, None, nat.ptr(eu),
+                                            nat.ptr(ev), None, nat.ptr(w), None), "graph export")
+        same = np.array_equal(eu, g.edge_u) and np.array_equal(ev, g.edge_v)
+        if same and w is not None:
+            same = g.sigma_g == float(info.sigma_g) and np.allclose(
+                w, g.edge_weights, rtol=1e-12, atol=0.0)
+    if not same:
+        raise GraphError("this stage runs on the device scan-line graph of the cloud; the "
+                         "given graph differs from it (other graphs: apply_filter/filter_step)")
+
+
+def build_knn_brute(pc: PointCloud, k: int) -> Graph:
+    """Exact k-nearest-neighbour graph by exhaustive search on the device
+    (graph.py:254-298): ties by point index, directed neighbour sets
+    symmetrised by union.  The bench-graph baseline (paper Table 3), off the
+    denoise path; integer or float coordinates."""
+    n = pc.n_points
+    k = int(k)
+    if not 1 <= k < n:
+        raise GraphError(f"k must satisfy 1 <= k < n_points, got k={k}, n={n}")
+    ctx = nat.context()
+    e = nat.c_i64()
+    q = pc.is_quantized
+    ctx.check(ctx.lib.fgbd_knn_build(ctx.handle, nat.ptr(pc.coords) if q else None,
+                                     None if q else nat.ptr(pc.coords), n, k,
+                                     int(pc.bit_depth) if q else 0, e, 0), "build_knn_brute")
+    ctx.graph_token = None  # the sort scratch was shared with the held SLG
+    m = int(e.value)
+    indptr = np.empty(n + 1, np.int64)
+    indices = np.empty(2 * m, np.int64)
+    csr_edge = np.empty(2 * m, np.int64)
+    eu = np.empty(m, np.int64)
+    ev = np.empty(m, np.int64)
+    sq = np.empty(m, np.float64)
+    ctx.check(ctx.lib.fgbd_knn_export(ctx.handle, nat.ptr(indptr), nat.ptr(indices),
+                                      nat.ptr(csr_edge), nat.ptr(eu), nat.ptr(ev), nat.ptr(sq)),
+              "knn export")
+    return Graph(n, indptr, indices, csr_edge, eu, ev, sq)

@@ -274,6 +274,10 @@ def _read(source):
         return buf[:got]
     if isinstance(source, (bytes, bytearray, memoryview)):
         return source
+    if isinstance(source, np.ndarray):  # raw file bytes, e.g. in pinned memory
+        if source.dtype != np.uint8 or source.ndim != 1:
+            raise TypeError("an array PLY source must be 1-D uint8 file bytes")
+        return source
     return source.read()
 
 
@@ -388,14 +392,17 @@ def write_ply(pc: PointCloud, path, fmt: str = "binary") -> None:
 
 def denoise_ply(source, cfg: FilterConfig = FilterConfig(), cached_q: int | None = None,
                 cached_sigma_est: float | None = None, *, fmt: str = "binary",
-                dest=None) -> tuple[bytes | None, DenoiseReport]:
+                dest=None, copy: bool = True) -> tuple[bytes | np.ndarray | None,
+                                                       DenoiseReport]:
     """`save_ply(denoise(load_ply(source), cfg, cached_q, cached_sigma_est)[0], fmt)`
     in one device pass for binary input with integer coordinates: the raw
     vertex records are uploaded, unpacked, denoised and re-packed on the GPU
     and only the 15-byte output records come back.  Other inputs (ascii,
     float coordinates, fewer than 2 points, ascii output) take the composed
     path.  With `dest` the result is written there and None is returned in
-    place of the bytes.
+    place of the bytes; with `copy=False` the fused path returns the file as a
+    read-only uint8 array in recycled page-locked memory instead of `bytes`
+    (no 15 B/pt host copy).
     """
     _check_fmt(fmt)
     data = _read(source)
@@ -436,4 +443,7 @@ def denoise_ply(source, cfg: FilterConfig = FilterConfig(), cached_q: int | None
         with open(dest, "wb") as fh:
             fh.write(memoryview(out))
         return None, report
+    if not copy:
+        out.flags.writeable = False
+        return out, report
     return out.tobytes(), report
