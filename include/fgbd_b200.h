@@ -295,6 +295,18 @@ int32_t fgbd_knn_build(fgbd_ctx* ctx, const int64_t* coords_int, const double* c
 int32_t fgbd_knn_export(fgbd_ctx* ctx, int64_t* indptr, int64_t* indices, int64_t* csr_edge,
                         int64_t* edge_u, int64_t* edge_v, double* edge_sqdist);
 
+/* ---- data-model helpers (cloud.py:89-140) --------- */
+/* quantize_coordinates: per-axis [min, max] -> [0, 2^bits - 1], rint.  One of
+ * coords_int / coords_float.  Integer clouds already on the grid are left
+ * alone: *passthrough = 1 and out is not written. */
+int32_t fgbd_quantize(fgbd_ctx* ctx, const int64_t* coords_int, const double* coords_float,
+                      int64_t n, int32_t bits, int64_t* out, int32_t* passthrough,
+                      uint32_t flags);
+/* sum over count values of (a - b)^2 in numpy's pairwise-summation order
+ * (np.mean's numerator in psnr, cloud.py:126-140). */
+int32_t fgbd_sq_error_sum(fgbd_ctx* ctx, const double* a, const double* b, int64_t count,
+                          double* sum_out, uint32_t flags);
+
 /* pinned host buffers for zero-staging transfers */
 void* fgbd_host_alloc(int64_t bytes);
 void fgbd_host_free(void* p);

@@ -199,6 +199,28 @@ def build_weighted_slg(coords, bit_depth) -> OracleGraph:
     return apply_gaussian_weights(g, compute_sigma_g(g))
 
 
+def quantize_coordinates(coords: np.ndarray, bits: int):
+    """cloud.py:89-108: per-axis affine map of [min, max] onto [0, 2^b - 1],
+    rint; integer clouds already on the grid pass through (returns None)."""
+    g = np.asarray(coords)
+    if np.issubdtype(g.dtype, np.integer) and g.min() >= 0 and g.max() < (1 << bits):
+        return None
+    lo = g.min(axis=0).astype(np.float64)
+    span = g.max(axis=0).astype(np.float64) - lo
+    scale = np.where(span > 0, ((1 << bits) - 1) / np.where(span > 0, span, 1.0), 0.0)
+    return np.rint((g - lo) * scale).astype(np.int64)
+
+
+def psnr(ref_colors: np.ndarray, test_colors: np.ndarray, cap_db: float = 100.0) -> float:
+    """cloud.py:126-140: pooled MSE over all 3N values (numpy's pairwise
+    summation in np.mean), 10 log10(255^2 / MSE), cap at zero error."""
+    diff = np.asarray(ref_colors, np.float64) - np.asarray(test_colors, np.float64)
+    mse = float(np.mean(diff * diff))
+    if mse == 0.0:
+        return float(cap_db)
+    return float(10.0 * np.log10(255.0 ** 2 / mse))
+
+
 def knn_rows(coords: np.ndarray, k: int, queries=None, chunk: int = 256) -> np.ndarray:
     """Exact k nearest neighbours (graph.py:254-285) for the given query rows.
 

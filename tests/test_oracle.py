@@ -12,11 +12,22 @@ from __future__ import annotations
 
 import math
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
 from conftest import cfg_kwargs, custom_input, digest, golden_case, golden_names, regen_input
 from oracle import fgbd_oracle as O
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def psnr_inputs(n: int):
+    """Same operands as tests/golden/make_cloud_golden.py (seed = n)."""
+    rng = np.random.default_rng(n)
+    a = rng.uniform(0, 255, size=(n, 3))
+    return a, np.clip(a + rng.normal(0, 9, size=(n, 3)), 0, 255)
 
 # ---------------------------------------------------------------------------
 # SPEC known answers
@@ -95,16 +106,24 @@ def test_spec_criterion_and_spectral():
 
 
 def test_spec_psnr_and_quantize():
-    from paper_2401_09721_b200 import PointCloud, psnr, quantize_coordinates
+    a = np.full((4, 3), 7.0)
+    assert O.psnr(a, a) == 100.0
+    assert O.psnr(np.zeros((4, 3)), np.full((4, 3), 255.0)) == 0.0
+    q = O.quantize_coordinates(np.array([[0.0, 0, 0], [1.0, 0, 0]]), 4)
+    assert q[:, 0].tolist() == [0, 15] and q[:, 1].tolist() == [0, 0]
+    assert O.quantize_coordinates(np.array([[0, 1, 2], [3, 4, 5]]), 3) is None
 
-    a = PointCloud(np.zeros((4, 3), np.int64), np.full((4, 3), 7.0), 2)
-    assert psnr(a, a) == 100.0
-    b = a.with_colors(np.full((4, 3), 7.0 + 255.0 - 7.0))
-    z = PointCloud(np.zeros((4, 3), np.int64), np.zeros((4, 3)), 2)
-    assert psnr(z, b.with_colors(np.full((4, 3), 255.0))) == 0.0
-    f = PointCloud(np.array([[0.0, 0, 0], [1.0, 0, 0]]), np.zeros((2, 3)))
-    q = quantize_coordinates(f, 4)
-    assert q.coords[:, 0].tolist() == [0, 15] and q.coords[:, 1].tolist() == [0, 0]
+
+def test_oracle_quantize_and_psnr_match_reference_fixture():
+    """Pinned to outputs of the reference's cloud.py (tests/golden/cloud.npz)."""
+    z = np.load(GOLDEN / "cloud.npz")
+    for name in sorted({k.split("/")[0] for k in z.files if k.endswith("/in")}):
+        got = O.quantize_coordinates(z[f"{name}/in"], int(z[f"{name}/bits"]))
+        want = z[f"{name}/out"]
+        assert np.array_equal(z[f"{name}/in"] if got is None else got, want), name
+    for name in sorted({k.split("/")[0] for k in z.files if k.endswith("/psnr")}):
+        a, b = psnr_inputs(int(name.split("_")[1]))
+        assert O.psnr(a, b) == float(z[f"{name}/psnr"]), name
 
 
 def test_eigensolver_suite_oracle():
