@@ -320,7 +320,7 @@ def run_b200(args):
                                                  "n_edges": int(rep0.n_edges)}),
             "mpoints_per_s": world * args.steps * n / (total_ms / 1e3) / 1e6,
             "stage_ms": stage,
-            "roofline": {"bound": "hbm", "kernel": "k_lf_step",
+            "roofline": {"bound": "hbm", "kernel": "k_lf_run",
                          "achieved": lf_bytes / lf_s / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": lf_bytes / lf_s / 1e9 / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": lf_bytes,

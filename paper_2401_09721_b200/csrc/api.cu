@@ -362,6 +362,8 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_L2_PERSIST")) ctx->l2_persist = std::atoi(v);
   if (const char* v = std::getenv("FGBD_NE_VARIANT")) ctx->ne_variant = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_SHAPE")) ctx->lf_shape = std::atoi(v) & 3;
+  if (const char* v = std::getenv("FGBD_LF_CHUNK")) ctx->lf_chunk = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_LF_HALO")) ctx->lf_halo = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (ensure_capacity(ctx, max_points > 0 ? max_points : 1, 0) != FGBD_OK) {
     set_error(nullptr, FGBD_E_CUDA, ctx->err);
@@ -386,6 +388,7 @@ void fgbd_ctx_destroy(fgbd_ctx* ctx) {
   if (ctx->csr_scratch) cudaFree(ctx->csr_scratch);
   if (ctx->ply_stage) cudaFree(ctx->ply_stage);
   if (ctx->aux) cudaFree(ctx->aux);
+  if (ctx->p2p_flags) cudaFree(ctx->p2p_flags);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->side) cudaStreamSynchronize(ctx->side);

@@ -120,7 +120,9 @@ struct fgbd_ctx {
   unsigned int* tickets = nullptr;  // group tickets for hierarchical reductions
   int lf_variant = 10;          // filter-step kernel (FGBD_LF_VARIANT): 0 per-step, 2+ persistent
   int coop_blocks[64] = {};      // co-resident grid of each persistent instantiation
-  int lf_shape = 0;             // persistent kernel block shape (FGBD_LF_SHAPE)
+  int lf_shape = 0;
+  int lf_halo = 128;  // FGBD_LF_HALO: window rows either side of a TMA tile
+  int lf_chunk = 1;  // FGBD_LF_CHUNK: contiguous row range per block (0 = grid-stride)             // persistent kernel block shape (FGBD_LF_SHAPE)
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)
@@ -132,6 +134,8 @@ struct fgbd_ctx {
   void* csr_scratch = nullptr;
   void* ply_stage = nullptr;     // PLY records in/out (fgbd_denoise_ply)
   size_t ply_stage_bytes = 0;
+  unsigned long long* p2p_flags = nullptr;  // persistent-kernel step flags (lf_variant 13)
+  unsigned long long p2p_epoch = 1ull << 20;
   void* aux = nullptr;           // off-path scratch (kNN graph), grown on demand
   size_t aux_bytes = 0;
   int64_t knn_n = -1, knn_e = 0;  // kNN graph held in aux

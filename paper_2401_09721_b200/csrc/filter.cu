@@ -23,10 +23,20 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <climits>
 #include <type_traits>
 #include <cmath>
 #include <vector>
 
+#ifndef FGBD_LF_DENSE
+#define FGBD_LF_DENSE 1
+#endif
+#ifndef FGBD_ELL_POLICY
+#define FGBD_ELL_POLICY 0  // L2 policy of the per-step graph stream: 0 evict_first, 1 evict_last, 2 normal
+#endif
+#ifndef FGBD_LF_SIGHINT
+#define FGBD_LF_SIGHINT 1
+#endif
 #include "device_util.cuh"
 #include "fgbd_internal.cuh"
 
@@ -185,7 +195,41 @@ struct StepArgs {
   double* part;  // [2 parities][3][grid]
   Ctl* ctl;
   int fixed_steps;  // cached path: number of steps (Y -> A/B ping-pong)
+  int64_t chunk;    // persistent kernels: rows per block (contiguous), 0 = grid-stride
+  int halo;         // TMA-staged sweep: window rows either side of a row tile
+  unsigned long long* flags;  // P2P: per-block "step published" words (monotone across launches)
+  unsigned long long base;    // P2P: this launch's flag base (published value = base + step)
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Spin until flags[b] >= want for every b in [lo, hi] except `self`.
+__device__ __forceinline__ void wait_blocks(const unsigned long long* flags, int lo, int hi,
+                                            int self, unsigned long long want) {
+  if (lo > hi) return;  // a block without rows depends on nobody
+  for (int b = lo + (int)threadIdx.x; b <= hi; b += blockDim.x) {
+    if (b == self) continue;
+    while (ld_acquire_u64(flags + b) < want) __nanosleep(20);
+  }
+}
+
+__device__ __forceinline__ uint64_t graph_policy() {
+#if FGBD_ELL_POLICY == 1
+  return policy_evict_last();
+#elif FGBD_ELL_POLICY == 2
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+#else
+  return policy_evict_first();
+#endif
+}
 
 // Where a row's six weights come from.
 enum WMode { W_STORED = 0, W_COORDS32 = 1, W_COORDS64 = 2 };
@@ -236,10 +280,32 @@ __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const
                                                   const double4* in, int64_t i, uint64_t pol_keep) {
   const double4 f = ld_row_hint(in + i, pol_keep);
   double4 g[kSlots];
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
+#if FGBD_LF_DENSE
+  // Every slot is gathered and accumulated: padding slots are (self, 0.0)
+  // and zero-weight edges add +0.0 * f_j = +0.0 to a non-negative
+  // accumulator, which leaves it bit-identical -- and the row has no
+  // per-slot branches.
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s)
+#if FGBD_LF_SIGHINT
+    g[s] = ld_row_hint(in + nb[s], pol_keep);
+#else
+    g[s] = ld_row(in + nb[s]);
+#endif
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    const double w = (double)wf[s];
+    lo = __dadd_rn(lo, nb[s] < (int)i ? w : 0.0);
+    hi = __dadd_rn(hi, nb[s] > (int)i ? w : 0.0);
+    acc0 = __dadd_rn(acc0, __dmul_rn(w, g[s].x));
+    acc1 = __dadd_rn(acc1, __dmul_rn(w, g[s].y));
+    acc2 = __dadd_rn(acc2, __dmul_rn(w, g[s].z));
+  }
+#else
 #pragma unroll
   for (int s = 0; s < kSlots; ++s)
     g[s] = (wf[s] != 0.0f) ? ld_row_hint(in + nb[s], pol_keep) : make_double4(0, 0, 0, 0);
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
     const double w = (double)wf[s];
@@ -251,6 +317,7 @@ __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const
       acc2 = __dadd_rn(acc2, __dmul_rn(w, g[s].z));
     }
   }
+#endif
   const double d = __dadd_rn(hi, lo);
   if (d == 0.0) return f;
   const double d2 = __dmul_rn(2.0, d);
@@ -327,20 +394,31 @@ template <int WM, bool SUMS>
 __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, double4* out,
                                       bool mask_all, float neg_inv_sg2, double (&sx)[3]) {
   const int64_t n = a.n;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // rows of this block: a contiguous range walked in blockDim strides (the
+  // neighbours of raster / scan-ordered clouds then mostly hit this SM's L1),
+  // or the grid-stride interleave
+  int64_t i, end, stride;
+  if (a.chunk > 0) {
+    i = (int64_t)blockIdx.x * a.chunk + threadIdx.x;
+    end = min(n, (int64_t)(blockIdx.x + 1) * a.chunk);
+    stride = blockDim.x;
+  } else {
+    i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    end = n;
+    stride = (int64_t)gridDim.x * blockDim.x;
+  }
+  const uint64_t pol_stream = graph_policy(), pol_keep = policy_evict_last();
   int nbc[kSlots], nbn[kSlots];
   float wc[kSlots], wn[kSlots];
-  if (i < n) load_row_slots<WM>(a, i, pol_stream, neg_inv_sg2, nbn, wn);
-  while (i < n) {
+  if (i < end) load_row_slots<WM>(a, i, pol_stream, neg_inv_sg2, nbn, wn);
+  while (i < end) {
 #pragma unroll
     for (int s = 0; s < kSlots; ++s) {
       nbc[s] = nbn[s];
       wc[s] = wn[s];
     }
     const int64_t inext = i + stride;
-    if (inext < n) load_row_slots<WM>(a, inext, pol_stream, neg_inv_sg2, nbn, wn);
+    if (inext < end) load_row_slots<WM>(a, inext, pol_stream, neg_inv_sg2, nbn, wn);
     const double4 o = row_from_slots(nbc, wc, in, i, pol_keep);
     st_row_hint(out + i, o, pol_keep);
     if (SUMS && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
@@ -350,6 +428,165 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
     }
     i = inext;
   }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged sweep (lf_variant 12).  A block walks its contiguous row range in
+// tiles of kTile rows, double-buffered through shared memory by the bulk-copy
+// engine (cp.async.bulk + mbarrier): per tile, the signal window
+// [c0 - halo, c1 + halo) and the tile's three ELL slot-pair planes.  A row's
+// own value and every neighbour inside the window come from shared memory;
+// only neighbours outside it (for raster-ordered clouds: the scan-line-3
+// ones) are gathered from global memory.  The tile after the current one is
+// in flight while the current one computes, without costing registers.
+// ---------------------------------------------------------------------------
+constexpr int kTile = 256;
+constexpr int kHaloMax = 128;
+constexpr int kWinRows = kTile + 2 * kHaloMax;
+constexpr int kStageBytes = kWinRows * 32 + 3 * kTile * 16;
+constexpr int kTmaSmem = 128 + 2 * kStageBytes;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+struct TmaState {
+  uint64_t* bar;        // [2]
+  unsigned char* stage; // [2][kStageBytes]
+  uint32_t uses[2];     // completed phases per stage (uniform over the block)
+};
+
+__device__ __forceinline__ void tma_issue(const StepArgs& a, const double4* in, TmaState& t,
+                                          int st, int64_t c0, int64_t c1, uint64_t pol_stream,
+                                          uint64_t pol_keep) {
+  const int64_t n = a.n;
+  const int64_t w0 = c0 - a.halo > 0 ? c0 - a.halo : 0;
+  const int64_t w1 = c1 + a.halo < n ? c1 + a.halo : n;
+  const uint32_t wb = (uint32_t)((w1 - w0) * 32), eb = (uint32_t)((c1 - c0) * 16);
+  unsigned char* base = t.stage + st * kStageBytes;
+  mbar_expect_tx(&t.bar[st], wb + 3 * eb);
+  bulk_g2s(base, in + w0, wb, &t.bar[st], pol_keep);
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+    bulk_g2s(base + kWinRows * 32 + p * kTile * 16, a.E.nbr + (int64_t)p * 4 * n + 4 * c0, eb,
+             &t.bar[st], pol_stream);
+}
+
+template <bool SUMS>
+__device__ __forceinline__ void sweep_tma(const StepArgs& a, const double4* in, double4* out,
+                                          bool mask_all, TmaState& t, double (&sx)[3]) {
+  const int64_t n = a.n;
+  const int64_t lo = (int64_t)blockIdx.x * a.chunk;
+  const int64_t hi = min(n, lo + a.chunk);
+  const uint64_t pol_stream = graph_policy(), pol_keep = policy_evict_last();
+  const int tiles = hi > lo ? (int)((hi - lo + kTile - 1) / kTile) : 0;
+  if (threadIdx.x == 0 && tiles > 0) {
+    fence_proxy_async_global();  // last step's generic stores -> this step's bulk reads
+    tma_issue(a, in, t, 0, lo, min(hi, lo + kTile), pol_stream, pol_keep);
+  }
+  // tile k lives in stage (k & 1); stage 0 always takes tile 0 of a step
+  uint32_t u0 = t.uses[0], u1 = t.uses[1];
+  for (int k = 0; k < tiles; ++k) {
+    const int st = k & 1;
+    const int64_t c0 = lo + (int64_t)k * kTile, c1 = min(hi, c0 + kTile);
+    if (threadIdx.x == 0 && k + 1 < tiles)
+      tma_issue(a, in, t, st ^ 1, c1, min(hi, c1 + kTile), pol_stream, pol_keep);
+    const uint32_t par = (st ? u1 : u0) & 1;
+    mbar_wait(&t.bar[st], par);
+    if (st) ++u1; else ++u0;
+    const int64_t i = c0 + threadIdx.x;
+    if (i < c1) {
+      const int64_t w0 = c0 - a.halo > 0 ? c0 - a.halo : 0;
+      const int64_t w1 = c1 + a.halo < n ? c1 + a.halo : n;
+      const unsigned char* base = t.stage + st * kStageBytes;
+      const double4* W = reinterpret_cast<const double4*>(base);
+      const int4* E = reinterpret_cast<const int4*>(base + kWinRows * 32);
+      int nb[kSlots];
+      float wf[kSlots];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const int4 pr = E[p * kTile + threadIdx.x];
+        nb[2 * p] = pr.x;
+        wf[2 * p] = __int_as_float(pr.y);
+        nb[2 * p + 1] = pr.z;
+        wf[2 * p + 1] = __int_as_float(pr.w);
+      }
+      // far neighbours first (global), then the window (shared)
+      double4 g[kSlots];
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {
+        const bool near = nb[s] >= w0 && nb[s] < w1;
+        g[s] = (wf[s] != 0.0f && !near) ? ld_row_hint(in + nb[s], pol_keep)
+                                        : make_double4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {
+        const bool near = nb[s] >= w0 && nb[s] < w1;
+        if (wf[s] != 0.0f && near) g[s] = W[nb[s] - w0];
+      }
+      const double4 f = W[i - w0];
+      double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, dlo = 0.0, dhi = 0.0;
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {
+        const double w = (double)wf[s];
+        if (nb[s] < (int)i) dlo = __dadd_rn(dlo, w);
+        else if (nb[s] > (int)i) dhi = __dadd_rn(dhi, w);
+        if (wf[s] != 0.0f) {
+          acc0 = __dadd_rn(acc0, __dmul_rn(w, g[s].x));
+          acc1 = __dadd_rn(acc1, __dmul_rn(w, g[s].y));
+          acc2 = __dadd_rn(acc2, __dmul_rn(w, g[s].z));
+        }
+      }
+      const double d = __dadd_rn(dhi, dlo);
+      double4 o = f;
+      if (d != 0.0) {
+        const double d2 = __dmul_rn(2.0, d);
+        o = make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
+                         __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
+                         __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
+      }
+      st_row_hint(out + i, o, pol_keep);
+      if (SUMS && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+        sx[0] = fma(o.x, o.x, sx[0]);
+        sx[1] = fma(o.y, o.y, sx[1]);
+        sx[2] = fma(o.z, o.z, sx[2]);
+      }
+    }
+    __syncthreads();  // stage st is refilled by the issue at k + 1 (tile k + 2)
+  }
+  t.uses[0] = u0;
+  t.uses[1] = u1;
 }
 
 // The whole filter-step loop in ONE cooperative launch.
@@ -366,16 +603,53 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
 // the same partials in the same order, so all reach the same decision.  A
 // stop decided at c discards the speculative x_{c+1}; q_max stops never
 // compute it.
-template <int WM, bool SELECT, int BLK = kBlock, int MINB = 3>
+// P2P = true replaces the grid barrier by neighbourhood waits: a block's
+// rows reference (symmetric graph) only rows owned by the blocks in its
+// dependency range [dep_lo, dep_hi], computed from its ELL rows at entry.
+// Step c+1 may start once those blocks published step c (which also means
+// they finished reading the buffer this block is about to overwrite); the
+// criterion decision for step c waits for every block's step-c flag, one
+// step later, and reads partials from a 4-deep ring (no block is more than
+// two steps ahead of any other).
+template <int WM, bool SELECT, int BLK = kBlock, int MINB = 3, bool TMA = false,
+          bool P2P = false>
 __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  TmaState tma{reinterpret_cast<uint64_t*>(dyn_smem), dyn_smem + 128, {0u, 0u}};
+  if (TMA && threadIdx.x == 0) {
+    mbar_init(&tma.bar[0], 1);
+    mbar_init(&tma.bar[1], 1);
+  }
   __shared__ double s_red[32 * 3];
   __shared__ SelState s_st;
   __shared__ double s_sy[3], s_sv2;
   __shared__ long long s_inc;
   __shared__ int s_qmax, s_mode, s_early, s_mask_all;
+  __shared__ int s_dep_lo, s_dep_hi;
   Ctl* ctl = a.ctl;
   const int nb = gridDim.x;
+  constexpr int kRing = P2P ? 4 : 2;
+  if (P2P) {
+    if (threadIdx.x == 0) {
+      s_dep_lo = INT_MAX;
+      s_dep_hi = -1;
+    }
+    __syncthreads();
+    const int64_t lo = (int64_t)blockIdx.x * a.chunk, hi = min(a.n, lo + a.chunk);
+    int mn = INT_MAX, mx = -1;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {
+        const int j = __ldg(a.E.nbr + eslot(s, a.n, i));
+        mn = min(mn, j);
+        mx = max(mx, j);
+      }
+    if (mx >= 0) {
+      atomicMin(&s_dep_lo, (int)(mn / a.chunk));
+      atomicMax(&s_dep_hi, (int)(mx / a.chunk));
+    }
+  }
   if (threadIdx.x == 0) {
     if (SELECT) {
       s_st = SelState{ctl->q, ctl->best_q, ctl->streak, ctl->stop, ctl->in_buf, ctl->out_buf,
@@ -409,15 +683,27 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     if (ob == ib || ob == bb) ob = BUF_Y;
     if (c < s_qmax) {
       double sx[3] = {0.0, 0.0, 0.0};
-      sweep<WM, SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx);
+      if (TMA)
+        sweep_tma<SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, tma, sx);
+      else
+        sweep<WM, SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx);
       if (SELECT) {
         block_sum<3>(sx, s_red);
         if (threadIdx.x == 0)
-          for (int k = 0; k < 3; ++k) a.part[((c + 1) & 1) * 3 * nb + k * nb + blockIdx.x] = sx[k];
+          for (int k = 0; k < 3; ++k)
+            a.part[((c + 1) & (kRing - 1)) * 3 * nb + k * nb + blockIdx.x] = sx[k];
       }
     }
+    if (P2P) {  // publish step c + 1 (rows and partials)
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_u64(a.flags + blockIdx.x, a.base + c + 1);
+    }
     if (SELECT && !decided) {
-      const double* part = a.part + (c & 1) * 3 * nb;
+      if (P2P) {
+        wait_blocks(a.flags, 0, nb - 1, blockIdx.x, a.base + c);
+        __syncthreads();
+      }
+      const double* part = a.part + (c & (kRing - 1)) * 3 * nb;
       double t[3] = {0.0, 0.0, 0.0};
       for (int b = threadIdx.x; b < nb; b += blockDim.x)
 #pragma unroll
@@ -434,7 +720,13 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     }
     if (!SELECT && c >= s_qmax) break;
     if (s_st.stop) break;
-    grid.sync();
+    if (P2P) {
+      // x_{c+1} of every block this one reads (and that reads this one) is
+      // published; the acquire orders this block's next loads after it
+      wait_blocks(a.flags, s_dep_lo, s_dep_hi, blockIdx.x, a.base + c + 1);
+    } else {
+      grid.sync();
+    }
     if (threadIdx.x == 0) {
       s_st.in_b = ob;
       s_st.out_b = ob;
@@ -478,7 +770,7 @@ __global__ void __launch_bounds__(kBlock) k_lf_step(StepArgs a, int fin, int fou
   }
   const int64_t n = a.n;
   double sx[3] = {0.0, 0.0, 0.0};
-  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+  const uint64_t pol_stream = graph_policy(), pol_keep = policy_evict_last();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     double4 o;
@@ -643,18 +935,36 @@ static StepArgs step_args(fgbd_ctx* ctx, int64_t n) {
   return a;
 }
 
-template <int WM, bool SELECT, int BLK, int MINB>
+template <int WM, bool SELECT, int BLK, int MINB, bool TMA = false, bool P2P = false>
 static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
-  auto kern = k_lf_run<WM, SELECT, BLK, MINB>;
+  auto kern = k_lf_run<WM, SELECT, BLK, MINB, TMA, P2P>;
+  const int smem = TMA ? kTmaSmem : 0;
   if (ctx->coop_blocks[slot] == 0) {
+    if (TMA) {
+      FGBD_CUDA(ctx, cudaFuncSetAttribute((const void*)kern,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      FGBD_CUDA(ctx, cudaFuncSetAttribute((const void*)kern,
+                                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
     int per_sm = 0;
-    FGBD_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLK, 0));
+    FGBD_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLK, smem));
     ctx->coop_blocks[slot] = std::max(1, per_sm) * ctx->num_sms;
   }
   const int grid = (int)std::max<int64_t>(
       1, std::min<int64_t>((a.n + BLK - 1) / BLK, ctx->coop_blocks[slot]));
+  a.chunk = (TMA || P2P || ctx->lf_chunk) ? ((a.n + grid - 1) / grid + BLK - 1) / BLK * BLK : 0;
+  a.halo = std::min(ctx->lf_halo, kHaloMax);
+  if (P2P) {
+    if (!ctx->p2p_flags) {
+      FGBD_CUDA(ctx, cudaMalloc(&ctx->p2p_flags, 8192 * sizeof(unsigned long long)));
+      FGBD_CUDA(ctx, cudaMemset(ctx->p2p_flags, 0, 8192 * sizeof(unsigned long long)));
+    }
+    a.flags = ctx->p2p_flags;
+    a.base = ctx->p2p_epoch;
+    ctx->p2p_epoch += 1ull << 20;
+  }
   void* args[] = {&a};
-  FGBD_CUDA(ctx, cudaLaunchCooperativeKernel((void*)kern, grid, BLK, args, 0, ctx->stream));
+  FGBD_CUDA(ctx, cudaLaunchCooperativeKernel((void*)kern, grid, BLK, args, smem, ctx->stream));
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
 }
@@ -679,6 +989,10 @@ static int launch_run_any(fgbd_ctx* ctx, StepArgs& a) {
   if (ctx->lf_variant == 11)
     return 3 * ctx->g_bits <= 32 ? launch_run<W_COORDS32, SELECT>(ctx, a)
                                  : launch_run<W_COORDS64, SELECT>(ctx, a);
+  if (ctx->lf_variant == 12)  // TMA-staged row tiles (slot 40 + SELECT)
+    return launch_run_k<W_STORED, SELECT, kTile, 3, true>(ctx, a, 40 + (SELECT ? 1 : 0));
+  if (ctx->lf_variant == 13)  // neighbourhood flags instead of the grid barrier
+    return launch_run_k<W_STORED, SELECT, kBlock, 3, false, true>(ctx, a, 42 + (SELECT ? 1 : 0));
   return launch_run<W_STORED, SELECT>(ctx, a);
 }
 
