@@ -15,7 +15,7 @@ value      device-resident throughput: inputs already in HBM, the C-ABI call
 e2e        the public API `paper_2401_09721_b200.denoise(PointCloud)` with
            inputs in pinned host memory: H2D of coords+colours and D2H of the
            denoised colours inside every timed step.
-roofline   dominant kernel k_lf_step (the random-walk step): SURVEY 8(d)
+roofline   dominant kernel k_lf_run (the persistent random-walk step loop): SURVEY 8(d)
            algorithmic bytes per step (52.125 N + 8 nnz) / its mean event-timed
            duration, against MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline  the CPU oracle port (oracle/fgbd_oracle.py, numpy, the

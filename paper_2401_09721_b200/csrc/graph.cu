@@ -20,6 +20,10 @@
 #include "device_util.cuh"
 #include "fgbd_internal.cuh"
 
+#ifndef FGBD_SORT_MINB
+#define FGBD_SORT_MINB 3
+#endif
+
 namespace fgbd {
 
 // ---------------------------------------------------------------------------
@@ -139,7 +143,7 @@ constexpr unsigned long long kFlagAgg = 1ull << 32;
 constexpr unsigned long long kFlagPre = 2ull << 32;
 
 template <typename K, bool FIRST, bool LAST, bool SLG>
-__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(SortPass p) {
+__global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortPass p) {
   extern __shared__ __align__(16) unsigned char smem[];
   K* s_keys = reinterpret_cast<K*>(smem);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kSortTile);
