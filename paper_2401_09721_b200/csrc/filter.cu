@@ -197,6 +197,7 @@ struct StepArgs {
   int fixed_steps;  // cached path: number of steps (Y -> A/B ping-pong)
   int64_t chunk;    // persistent kernels: rows per block (contiguous), 0 = grid-stride
   int halo;         // TMA-staged sweep: window rows either side of a row tile
+  int exp;          // timing experiments only (FGBD_LF_EXP): 1 no sums, 2 no reduction, 4 two-buffer rotation
   unsigned long long* flags;  // P2P: per-block "step published" words (monotone across launches)
   unsigned long long base;    // P2P: this launch's flag base (published value = base + step)
 };
@@ -421,7 +422,7 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
     if (inext < end) load_row_slots<WM>(a, inext, pol_stream, neg_inv_sg2, nbn, wn);
     const double4 o = row_from_slots(nbc, wc, in, i, pol_keep);
     st_row_hint(out + i, o, pol_keep);
-    if (SUMS && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+    if (SUMS && !(a.exp & 1) && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
       sx[0] = fma(o.x, o.x, sx[0]);
       sx[1] = fma(o.y, o.y, sx[1]);
       sx[2] = fma(o.z, o.z, sx[2]);
@@ -440,6 +441,7 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
 // ones) are gathered from global memory.  The tile after the current one is
 // in flight while the current one computes, without costing registers.
 // ---------------------------------------------------------------------------
+constexpr int kMaxCoopBlocks = 592;  // persistent grids: <= 148 SMs x 4 blocks
 constexpr int kTile = 256;
 constexpr int kHaloMax = 128;
 constexpr int kWinRows = kTile + 2 * kHaloMax;
@@ -627,6 +629,13 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   __shared__ long long s_inc;
   __shared__ int s_qmax, s_mode, s_early, s_mask_all;
   __shared__ int s_dep_lo, s_dep_hi;
+  // step c's block partials land here by bulk copy while step c+1 sweeps
+  constexpr bool kBulkPart = SELECT && !P2P;
+  __shared__ __align__(16) double s_part[kBulkPart ? 3 * kMaxCoopBlocks + 2 : 2];
+  __shared__ __align__(8) uint64_t s_pbar;
+  uint32_t pbar_uses = 0;
+  const int pstride = (3 * gridDim.x + 1) & ~1;  // 16-byte aligned slots
+  if (kBulkPart && threadIdx.x == 0) mbar_init(&s_pbar, 1);
   Ctl* ctl = a.ctl;
   const int nb = gridDim.x;
   constexpr int kRing = P2P ? 4 : 2;
@@ -677,7 +686,13 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   int c = s_st.q;  // x_c complete and decided (c = 0 at entry)
   bool decided = true;
   while (!s_st.stop) {
-    const int ib = s_st.in_b, bb = s_st.best_b;
+    if (kBulkPart && !decided && threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)(pstride * 8);
+      fence_proxy_async_global();  // the partials were stored before the barrier
+      mbar_expect_tx(&s_pbar, bytes);
+      bulk_g2s(s_part, a.part + (c & 1) * pstride, bytes, &s_pbar, policy_evict_last());
+    }
+    const int ib = s_st.in_b, bb = (a.exp & 4) ? ib : s_st.best_b;
     int ob = BUF_A;
     if (ob == ib || ob == bb) ob = BUF_B;
     if (ob == ib || ob == bb) ob = BUF_Y;
@@ -691,7 +706,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
         block_sum<3>(sx, s_red);
         if (threadIdx.x == 0)
           for (int k = 0; k < 3; ++k)
-            a.part[((c + 1) & (kRing - 1)) * 3 * nb + k * nb + blockIdx.x] = sx[k];
+            a.part[((c + 1) & (kRing - 1)) * (kBulkPart ? pstride : 3 * nb) + k * nb + blockIdx.x] =
+                sx[k];
       }
     }
     if (P2P) {  // publish step c + 1 (rows and partials)
@@ -705,10 +721,20 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       }
       const double* part = a.part + (c & (kRing - 1)) * 3 * nb;
       double t[3] = {0.0, 0.0, 0.0};
-      for (int b = threadIdx.x; b < nb; b += blockDim.x)
+      if (!(a.exp & 2)) {
+        if (kBulkPart) {
+          mbar_wait(&s_pbar, pbar_uses & 1);
+          ++pbar_uses;
+          for (int b = threadIdx.x; b < nb; b += blockDim.x)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) t[k] += __ldcg(&part[k * nb + b]);
-      block_sum<3>(t, s_red);
+            for (int k = 0; k < 3; ++k) t[k] += s_part[k * nb + b];
+        } else {
+          for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) t[k] += __ldcg(&part[k * nb + b]);
+        }
+        block_sum<3>(t, s_red);
+      }
       if (threadIdx.x == 0) {
         const double crit = criterion(s_sy, t, s_inc, s_sv2, s_mode);
         s_st.out_b = s_st.in_b;  // x_c's buffer becomes the best if crit_c improves
@@ -951,9 +977,11 @@ static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
     ctx->coop_blocks[slot] = std::max(1, per_sm) * ctx->num_sms;
   }
   const int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>((a.n + BLK - 1) / BLK, ctx->coop_blocks[slot]));
+      1, std::min<int64_t>(std::min<int64_t>((a.n + BLK - 1) / BLK, ctx->coop_blocks[slot]),
+                           kMaxCoopBlocks));
   a.chunk = (TMA || P2P || ctx->lf_chunk) ? ((a.n + grid - 1) / grid + BLK - 1) / BLK * BLK : 0;
   a.halo = std::min(ctx->lf_halo, kHaloMax);
+  a.exp = ctx->lf_exp;
   if (P2P) {
     if (!ctx->p2p_flags) {
       FGBD_CUDA(ctx, cudaMalloc(&ctx->p2p_flags, 8192 * sizeof(unsigned long long)));

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--sigma", type=float, default=10.0)
     ap.add_argument("--frames", type=int, default=3)
     ap.add_argument("--cached", type=int, default=-1)
+    ap.add_argument("--no-early-exit", action="store_true")
     a = ap.parse_args()
     import torch
 
@@ -37,7 +38,7 @@ def main():
     dc = torch.from_numpy(np.array(noisy.coords)).cuda()
     dy = torch.from_numpy(np.array(noisy.colors)).cuda()
     do = torch.empty_like(dy)
-    cfg = nat.make_config(fb.FilterConfig())
+    cfg = nat.make_config(fb.FilterConfig(early_exit=not a.no_early_exit))
     for f in range(a.frames):
         rep = nat.Report()
         ctx.check(ctx.lib.fgbd_denoise(ctx.handle, dc.data_ptr(), dy.data_ptr(), a.n,
