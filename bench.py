@@ -61,6 +61,8 @@ def parse():
                          "slab: configs[4] (one frame split over the GPUs)")
     ap.add_argument("--frames", type=int, default=300, help="video length (configs[3])")
     ap.add_argument("--workers", type=int, default=2, help="host threads per GPU (video)")
+    ap.add_argument("--no-reuse", action="store_true",
+                    help="video/ply: rebuild the graph of every frame even when the geometry is static")
     return ap.parse_args()
 
 
@@ -434,7 +436,8 @@ def run_video(args):
 
     # warm-up: contexts for every worker thread, pinned output pool
     denoise_sequence(load, cfg, n_frames=min(2 * cfg.reestimate_interval, args.frames),
-                     workers=args.workers, process_group=pg, sink=sink)
+                     workers=args.workers, process_group=pg, sink=sink,
+                     reuse_graph=not args.no_reuse)
     if world > 1:
         import torch.distributed as dist
 
@@ -443,7 +446,7 @@ def run_video(args):
     compute.clear()
     t0 = time.perf_counter()
     res = denoise_sequence(load, cfg, n_frames=args.frames, workers=args.workers,
-                           process_group=pg, sink=sink)
+                           process_group=pg, sink=sink, reuse_graph=not args.no_reuse)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     if world > 1:
@@ -463,7 +466,10 @@ def run_video(args):
             "device_compute_ms_sum_per_frame": 1e3 * float(np.sum(compute)) / args.frames,
             "config": {"workload": "BASELINE.json configs[3]", "kind": args.kind,
                        "n_points": args.n, "sigma": args.sigma, "frames": args.frames,
-                       "rank0_heads": heads, "rank0_frames": len(res)},
+                       "rank0_heads": heads, "rank0_frames": len(res),
+                       "rank0_graph_reused": sum(1 for r in res.values()
+                                                 if r[1].device and r[1].device.get("graph_reused")),
+                       "geometry": "static (frames share the clean cloud's coordinates)"},
         }), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -504,7 +510,7 @@ def run_ply(args):
     cfg = fb.FilterConfig()
     load = lambda i: files[i % len(files)]
     fn = lambda src, cfg, cached_q=None, cached_sigma_est=None: denoise_ply(
-        src, cfg, cached_q, cached_sigma_est, copy=False)
+        src, cfg, cached_q, cached_sigma_est, copy=False, reuse_graph=not args.no_reuse)
     checksum = [0]
 
     compute = []
@@ -545,7 +551,10 @@ def run_ply(args):
                     "d2h_bytes_per_step": int(files[0].size)},
             "config": {"workload": "SURVEY 8(f) rank 2: PLY frame sequence", "kind": args.kind,
                        "n_points": args.n, "sigma": args.sigma, "frames": args.frames,
-                       "rank0_heads": heads, "rank0_frames": len(res)},
+                       "rank0_heads": heads, "rank0_frames": len(res),
+                       "rank0_graph_reused": sum(1 for r in res.values()
+                                                 if r[1].device and r[1].device.get("graph_reused")),
+                       "geometry": "static (frames share the clean cloud's coordinates)"},
         }), flush=True)
     if world > 1:
         import torch.distributed as dist

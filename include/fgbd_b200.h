@@ -54,6 +54,11 @@ enum {
 #define FGBD_FLAG_DEVICE_PTRS  0x1u  /* all array arguments are device pointers */
 #define FGBD_FLAG_WEIGHTS_F64  0x2u  /* keep edge weights in fp64 (parity mode)  */
 #define FGBD_FLAG_NO_TIMING    0x4u  /* skip per-stage CUDA events               */
+/* fgbd_denoise / fgbd_denoise_ply: if this context's last graph was built from
+ * byte-identical coordinates (same n and bit depth), reuse it instead of
+ * rebuilding (the SLG is a pure function of the coordinates; the check is an
+ * exact device-side comparison).  For static-geometry frame sequences. */
+#define FGBD_FLAG_REUSE_GRAPH  0x8u
 
 enum { FGBD_CRIT_POOLED = 0, FGBD_CRIT_PER_CHANNEL = 1 };   /* filtering.py:47 */
 enum { FGBD_TAU_COUNT = 0, FGBD_TAU_COUNT_PLUS_ONE = 1 };   /* filtering.py:49 */
@@ -107,6 +112,7 @@ typedef struct fgbd_report {
   double t_lf_steps;           /* seconds spent in the filter-step launches only */
   double t_h2d;                /* coordinates host->device (colours overlap the graph build) */
   double t_d2h;                /* denoised colours device->host */
+  int32_t graph_reused;        /* 1: FGBD_FLAG_REUSE_GRAPH matched the held graph */
 } fgbd_report;
 
 /* Result of NE-GBP (noise.py:63-73). */

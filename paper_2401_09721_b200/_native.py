@@ -24,6 +24,7 @@ FGBD_OK, E_CLOUD, E_GRAPH, E_NOISE, E_FILTER, E_CUDA, E_NCCL, E_ARG = range(8)
 FLAG_DEVICE_PTRS = 0x1
 FLAG_WEIGHTS_F64 = 0x2
 FLAG_NO_TIMING = 0x4
+FLAG_REUSE_GRAPH = 0x8
 MAX_PATCH = 7
 TRACE_MAX = 1025
 
@@ -53,7 +54,8 @@ class Report(C.Structure):
                 ("eigenvalues", (c_f64 * MAX_PATCH) * 3), ("tail_m", c_i32 * 3),
                 ("tail_tau", c_f64 * 3), ("tail_fallback", c_i32 * 3), ("n_trace", c_i32),
                 ("trace", c_f64 * TRACE_MAX), ("gpu_launches", c_i32),
-                ("t_lf_steps", c_f64), ("t_h2d", c_f64), ("t_d2h", c_f64)]
+                ("t_lf_steps", c_f64), ("t_h2d", c_f64), ("t_d2h", c_f64),
+                ("graph_reused", c_i32)]
 
 
 class Noise(C.Structure):

@@ -147,6 +147,14 @@ struct fgbd_ctx {
 
   // state of the graph held by the context
   int64_t g_n = -1;
+  // static-geometry reuse (FGBD_FLAG_REUSE_GRAPH): coordinates and header of
+  // the held graph
+  int64_t* held_coords = nullptr;  // 3 x held_cap int64
+  int64_t held_cap = 0;
+  int held_valid = 0;
+  unsigned long long held_edges = 0;
+  double held_sigma_g = 0.0;
+  int held_max_deg = 0;
   int g_bits = 0;
   int g_weights64 = 0;
   int g_have_weights = 0;

@@ -20,11 +20,16 @@
 #include "device_util.cuh"
 #include "fgbd_internal.cuh"
 
+#ifndef FGBD_LOOK_BATCH
+#define FGBD_LOOK_BATCH 4
+#endif
 #ifndef FGBD_SORT_MINB
 #define FGBD_SORT_MINB 3
 #endif
 
 namespace fgbd {
+
+constexpr int kLookBatch = FGBD_LOOK_BATCH;
 
 // ---------------------------------------------------------------------------
 // codes
@@ -219,14 +224,28 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
     atomicExch(&st[d], ep | kFlagPre | count);
   } else {
     atomicExch(&st[(int64_t)tile * kRadix + d], ep | kFlagAgg | count);
+    // look back kLookBatch predecessors per round: their status words are
+    // loaded together, then consumed newest-first until an inclusive prefix
     int k = tile - 1;
-    while (true) {
-      const unsigned long long v =
-          *reinterpret_cast<volatile unsigned long long*>(&st[(int64_t)k * kRadix + d]);
-      if ((v >> 34) != p.epoch || ((v >> 32) & 3ull) == 0) continue;
-      excl += (uint32_t)v;
-      if (((v >> 32) & 3ull) == 2) break;
-      --k;
+    bool done = false;
+    while (!done) {
+      unsigned long long v[kLookBatch];
+#pragma unroll
+      for (int j = 0; j < kLookBatch; ++j)
+        v[j] = k - j >= 0 ? *reinterpret_cast<volatile unsigned long long*>(
+                                &st[(int64_t)(k - j) * kRadix + d])
+                          : 0ull;
+#pragma unroll
+      for (int j = 0; j < kLookBatch; ++j) {
+        if (done) break;
+        if ((v[j] >> 34) != p.epoch || ((v[j] >> 32) & 3ull) == 0) {
+          k -= j;  // not published yet: re-read from this tile on
+          break;
+        }
+        excl += (uint32_t)v[j];
+        if (((v[j] >> 32) & 3ull) == 2) done = true;
+        if (j == kLookBatch - 1) k -= kLookBatch;
+      }
     }
     atomicExch(&st[(int64_t)tile * kRadix + d], ep | kFlagPre | (excl + count));
   }
@@ -672,6 +691,7 @@ int launch_graph(fgbd_ctx* ctx, int64_t n, int bits) {
   ctx->g_bits = bits;
   ctx->g_have_weights = 0;
   ctx->g_have_noise = 0;
+  ctx->held_valid = 0;  // a new graph: the reuse copy no longer describes it
   return FGBD_OK;
 }
 

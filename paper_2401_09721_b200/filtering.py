@@ -248,6 +248,7 @@ def _device_info(r: nat.Report, patch: int) -> dict:
         "t_lf_steps": float(r.t_lf_steps),
         "t_h2d": float(r.t_h2d),
         "t_d2h": float(r.t_d2h),
+        "graph_reused": bool(r.graph_reused),
     }
 
 
@@ -260,6 +261,16 @@ def denoise(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
     input unchanged; `cached_q` skips estimation and selection; geometry is
     never modified; an all-excluded FSLR mask warns and selects unmasked.
     """
+    return denoise_frame(pc_noisy, cfg, cached_q, cached_sigma_est)
+
+
+def denoise_frame(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
+                  cached_q: int | None = None, cached_sigma_est: float | None = None,
+                  reuse_graph: bool = False) -> tuple[PointCloud, DenoiseReport]:
+    """`denoise` for one frame of a sequence.  With `reuse_graph`, a frame
+    whose coordinates are byte-identical to the previous frame handled by
+    this thread's device context reuses that scan-line graph instead of
+    rebuilding it (verified on the device; results are identical)."""
     n = pc_noisy.n_points
     if n < 2:
         return pc_noisy, DenoiseReport(
@@ -274,7 +285,8 @@ def denoise(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
     cq = -1 if cached_q is None else int(cached_q)
     cs = float("nan") if cached_sigma_est is None else float(cached_sigma_est)
     ctx.check(ctx.lib.fgbd_denoise(ctx.handle, nat.ptr(pc_noisy.coords), nat.ptr(pc_noisy.colors),
-                                   n, bits, nat.make_config(cfg), cq, cs, nat.ptr(out), rep, 0),
+                                   n, bits, nat.make_config(cfg), cq, cs, nat.ptr(out), rep,
+                                   nat.FLAG_REUSE_GRAPH if reuse_graph else 0),
               "denoise")
     ctx.graph_token = None
     report = _report_from(rep, cfg, cached_q, cached_sigma_est)

@@ -392,8 +392,8 @@ def write_ply(pc: PointCloud, path, fmt: str = "binary") -> None:
 
 def denoise_ply(source, cfg: FilterConfig = FilterConfig(), cached_q: int | None = None,
                 cached_sigma_est: float | None = None, *, fmt: str = "binary",
-                dest=None, copy: bool = True) -> tuple[bytes | np.ndarray | None,
-                                                       DenoiseReport]:
+                dest=None, copy: bool = True,
+                reuse_graph: bool = False) -> tuple[bytes | np.ndarray | None, DenoiseReport]:
     """`save_ply(denoise(load_ply(source), cfg, cached_q, cached_sigma_est)[0], fmt)`
     in one device pass for binary input with integer coordinates: the raw
     vertex records are uploaded, unpacked, denoised and re-packed on the GPU
@@ -402,7 +402,7 @@ def denoise_ply(source, cfg: FilterConfig = FilterConfig(), cached_q: int | None
     path.  With `dest` the result is written there and None is returned in
     place of the bytes; with `copy=False` the fused path returns the file as a
     read-only uint8 array in recycled page-locked memory instead of `bytes`
-    (no 15 B/pt host copy).
+    (no 15 B/pt host copy).  `reuse_graph`: see `filtering.denoise_frame`.
     """
     _check_fmt(fmt)
     data = _read(source)
@@ -431,7 +431,8 @@ def denoise_ply(source, cfg: FilterConfig = FilterConfig(), cached_q: int | None
     rc = ctx.lib.fgbd_denoise_ply(ctx.handle, nat.ptr(body), n, blk.stride,
                                   blk.offsets.ctypes.data_as(nat.P(nat.c_i32)),
                                   blk.types.ctypes.data_as(nat.P(nat.c_i32)), 0,
-                                  nat.make_config(cfg), cq, cs, nat.ptr(out[head:]), rep, 0)
+                                  nat.make_config(cfg), cq, cs, nat.ptr(out[head:]), rep,
+                                  nat.FLAG_REUSE_GRAPH if reuse_graph else 0)
     if rc == nat.E_CLOUD:
         msg = ctx.lib.fgbd_last_error(ctx.handle).decode()
         if msg.startswith("negative"):

@@ -22,7 +22,9 @@ from dataclasses import dataclass
 from typing import Callable, Sequence
 
 from .cloud import PointCloud
-from .filtering import DenoiseReport, FilterConfig, denoise
+from functools import partial
+
+from .filtering import DenoiseReport, FilterConfig, denoise_frame
 
 
 @dataclass(frozen=True)
@@ -74,8 +76,9 @@ def _run_many(fn, items, workers):
 
 def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
                      cfg: FilterConfig = FilterConfig(), *, n_frames: int | None = None,
-                     workers: int = 2, process_group=None, denoise_fn=denoise,
+                     workers: int = 2, process_group=None, denoise_fn=None,
                      sink: Callable[[int, PointCloud, DenoiseReport], object] | None = None,
+                     reuse_graph: bool = True,
                      ) -> dict[int, tuple[PointCloud, DenoiseReport]]:
     """Denoise a frame sequence with the reference's every-K-frames q reuse.
 
@@ -86,7 +89,13 @@ def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
     returned.  `denoise_fn` defaults to the B200 `denoise`.  With `sink`, each
     finished frame is handed to `sink(index, cloud, report)` (e.g. a PLY
     writer) and only the reports are kept, so output buffers recycle.
+    With `reuse_graph` (default), a frame whose coordinates are byte-identical
+    to the previous frame of the same worker reuses that worker's scan-line
+    graph (static geometry; checked exactly on the device, results
+    unchanged; `report.device["graph_reused"]`).
     """
+    if denoise_fn is None:
+        denoise_fn = partial(denoise_frame, reuse_graph=reuse_graph)
     load = frames if callable(frames) else (lambda i: frames[i])
     n = n_frames if n_frames is not None else len(frames)  # type: ignore[arg-type]
     world, rank = 1, 0
