@@ -54,6 +54,7 @@ static void free_scratch(fgbd_ctx* ctx) {
   f(ctx->nbr);
   f(ctx->w64);
   f(ctx->meta);
+  f(ctx->pos);
   for (int k = 0; k < 3; ++k) {
     f(ctx->buf[k]);
     ctx->buf[k] = nullptr;
@@ -69,6 +70,9 @@ static void free_scratch(fgbd_ctx* ctx) {
   ctx->pay = nullptr;
   ctx->w64 = nullptr;
   ctx->meta = nullptr;
+  ctx->pos = nullptr;
+  ctx->rowid = nullptr;
+  ctx->g_reordered = 0;
   ctx->out = nullptr;
   ctx->fslr = nullptr;
   ctx->mask = nullptr;
@@ -101,6 +105,7 @@ int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64) {
   if ((rc = dalloc(ctx, &ctx->nbr, 2 * kSlots * cap))) return rc;
   ctx->pay = reinterpret_cast<uint32_t*>(ctx->nbr + 1);
   if ((rc = dalloc(ctx, &ctx->meta, cap))) return rc;
+  if ((rc = dalloc(ctx, &ctx->pos, cap))) return rc;
   for (int k = 0; k < 3; ++k)
     if ((rc = dalloc(ctx, &ctx->buf[k], 4 * cap))) return rc;
   if ((rc = dalloc(ctx, &ctx->out, 3 * cap))) return rc;
@@ -137,6 +142,8 @@ int upload_colors_async(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev
                                    cudaMemcpyHostToDevice, ctx->side));
     src = ctx->out;
   }
+  // reordered rows: the expansion gathers through the line-1 permutation
+  if (ctx->g_reordered) FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_perm, 0));
   int rc = launch_expand(ctx, src, n, BUF_Y, ctx->side);
   if (rc) return rc;
   FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->side));
@@ -296,7 +303,7 @@ int restore_graph_header(fgbd_ctx* ctx) {
 
 // Load a frame's coordinates and build the weighted scan-line graph.
 int stage_graph(fgbd_ctx* ctx, const int64_t* coords, int64_t n, int bits, bool dev, int w64,
-                bool weights = true) {
+                bool weights = true, bool reorder = false) {
   int rc = ensure_capacity(ctx, n, 3 * bits > 32);
   if (rc) return rc;
   if ((rc = reset_ctl(ctx))) return rc;
@@ -306,9 +313,11 @@ int stage_graph(fgbd_ctx* ctx, const int64_t* coords, int64_t n, int bits, bool 
     if ((rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false))) return rc;
     ctx->cur_coords = ctx->coords64;
   }
-  if ((rc = launch_graph(ctx, n, bits))) return rc;
+  if ((rc = launch_graph(ctx, n, bits, reorder))) return rc;
   return weights ? launch_weights(ctx, n, bits, w64) : FGBD_OK;
 }
+
+
 
 int check_graph_ctl(fgbd_ctx* ctx, int bits) {
   const Ctl& h = *ctx->ctl_host;
@@ -354,6 +363,19 @@ void fill_noise_report(fgbd_report* r, const fgbd_noise& nz) {
 
 }  // namespace
 
+namespace fgbd {
+// Stage entry points that exchange per-point arrays other than colours with
+// the caller (patches, masks, statistics, the CSR export) work on a graph
+// whose rows are in point order -- the one fgbd_build_graph holds.
+int require_point_rows(fgbd_ctx* ctx) {
+  if (ctx->g_reordered)
+    return set_error(ctx, FGBD_E_GRAPH,
+                     "the held graph comes from fgbd_denoise (rows in scan-line order); "
+                     "call fgbd_build_graph first");
+  return FGBD_OK;
+}
+}  // namespace fgbd
+
 extern "C" {
 
 int32_t fgbd_abi_version(void) { return FGBD_ABI_VERSION; }
@@ -397,6 +419,8 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
     return fail(e, "side stream");
   if ((e = cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming)) != cudaSuccess)
     return fail(e, "side event");
+  if ((e = cudaEventCreateWithFlags(&ctx->ev_perm, cudaEventDisableTiming)) != cudaSuccess)
+    return fail(e, "perm event");
   for (auto& ev : ctx->ev)
     if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(e, "event");
   if ((e = cudaMalloc(&ctx->ctl, sizeof(Ctl))) != cudaSuccess) return fail(e, "ctl");
@@ -414,6 +438,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_NE_VARIANT")) ctx->ne_variant = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_SHAPE")) ctx->lf_shape = std::atoi(v) & 3;
   if (const char* v = std::getenv("FGBD_LF_CHUNK")) ctx->lf_chunk = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_REORDER")) ctx->reorder_rows = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_EXP")) ctx->lf_exp = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_HALO")) ctx->lf_halo = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
@@ -446,6 +471,7 @@ void fgbd_ctx_destroy(fgbd_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   if (ctx->side) cudaStreamSynchronize(ctx->side);
   if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
+  if (ctx->ev_perm) cudaEventDestroy(ctx->ev_perm);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -555,7 +581,8 @@ static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coord
     if ((rc = restore_graph_header(ctx))) return rc;
     ctx->cur_coords = frame_coords;
   } else {
-    if ((rc = stage_graph(ctx, frame_coords, n, bits, true, w64, !fuse_w))) return rc;
+    if ((rc = stage_graph(ctx, frame_coords, n, bits, true, w64, !fuse_w, ctx->reorder_rows != 0)))
+      return rc;
     if (want_reuse && (rc = hold_coords(ctx, frame_coords, n))) return rc;
   }
   rep->graph_reused = reuse ? 1 : 0;
@@ -770,6 +797,7 @@ int32_t fgbd_graph_export(fgbd_ctx* ctx, int64_t* indptr, int64_t* indices, int6
   if (!ctx) return set_error(ctx, FGBD_E_ARG, "null context");
   cudaSetDevice(ctx->device);
   if (ctx->g_n < 0) return set_error(ctx, FGBD_E_GRAPH, "no graph held by this context");
+  if (int e = require_point_rows(ctx)) return e;
   const int64_t n = ctx->g_n;
   if (n < 2) {
     if (indptr)
@@ -822,6 +850,7 @@ int32_t fgbd_estimate_noise(fgbd_ctx* ctx, const double* colors, int32_t patch_s
   ctx->err.clear();
   std::memset(out, 0, sizeof(*out));
   if (ctx->g_n < 0) return set_error(ctx, FGBD_E_GRAPH, "no graph held by this context");
+  if (int e = require_point_rows(ctx)) return e;
   const int64_t n = ctx->g_n;
   const int D = patch_size;
   if (D < 2) return set_error(ctx, FGBD_E_NOISE, "patch_size must be >= 2, got " + std::to_string(D));
@@ -854,6 +883,7 @@ int32_t fgbd_fslr_mask(fgbd_ctx* ctx, double sigma_est, double sigma_floor, uint
   if (!ctx || !include_out) return set_error(ctx, FGBD_E_ARG, "null argument");
   cudaSetDevice(ctx->device);
   ctx->err.clear();
+  if (int e = require_point_rows(ctx)) return e;
   if (all_excluded) *all_excluded = 0;
   if (!ctx->g_have_noise)
     return set_error(ctx, FGBD_E_NOISE, "run fgbd_estimate_noise before fgbd_fslr_mask");
@@ -951,6 +981,7 @@ int32_t fgbd_select_q(fgbd_ctx* ctx, const double* colors, const uint8_t* includ
     return set_error(ctx, FGBD_E_FILTER, b);
   }
   if (ctx->g_n < 0) return set_error(ctx, FGBD_E_GRAPH, "no graph held by this context");
+  if (int e = require_point_rows(ctx)) return e;
   const int64_t n = ctx->g_n;
   const bool dev = flags & FGBD_FLAG_DEVICE_PTRS;
   if ((rc = upload_colors(ctx, colors, n, dev))) return rc;

@@ -41,6 +41,14 @@ __device__ __forceinline__ int64_t eslot(int s, int64_t n, int64_t i) {
   return (int64_t)(s >> 1) * 4 * n + 4 * i + 2 * (s & 1);
 }
 
+// An ELL neighbour word is the neighbour's ROW (position) in bits 0-30 and,
+// in bit 31, whether its ORIGINAL point index is below the row's own -- the
+// reference's weighted degree is (sum over j > i) + (sum over j < i) of the
+// original indices, whatever order the rows are stored in.
+constexpr int kBelowBit = (int)0x80000000u;
+__device__ __forceinline__ int ell_j(int v) { return v & 0x7fffffff; }
+__device__ __forceinline__ bool ell_below(int v) { return v < 0; }
+
 // Block-wide sum of NV doubles per thread; result valid in thread 0.
 // Fixed shuffle tree + fixed warp order => deterministic.
 template <int NV>

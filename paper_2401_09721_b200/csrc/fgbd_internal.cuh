@@ -123,7 +123,8 @@ struct fgbd_ctx {
   int lf_shape = 0;
   int lf_halo = 128;  // FGBD_LF_HALO: window rows either side of a TMA tile
   int lf_exp = 0;    // FGBD_LF_EXP: timing experiments (filter.cu StepArgs::exp)
-  int lf_chunk = 1;  // FGBD_LF_CHUNK: contiguous row range per block (0 = grid-stride)             // persistent kernel block shape (FGBD_LF_SHAPE)
+  int lf_chunk = 1;
+  int reorder_rows = 1;  // FGBD_REORDER: denoise-path rows in scan-line-1 order  // FGBD_LF_CHUNK: contiguous row range per block (0 = grid-stride)             // persistent kernel block shape (FGBD_LF_SHAPE)
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)
@@ -147,6 +148,10 @@ struct fgbd_ctx {
 
   // state of the graph held by the context
   int64_t g_n = -1;
+  int g_reordered = 0;            // rows of the held graph are in line-1 order
+  const uint32_t* rowid = nullptr;  // row -> point (line-1 perm) when reordered
+  int* pos = nullptr;             // point -> row (cap)
+  cudaEvent_t ev_perm = nullptr;  // line-1 permutation ready (main stream)
   // static-geometry reuse (FGBD_FLAG_REUSE_GRAPH): coordinates and header of
   // the held graph
   int64_t* held_coords = nullptr;  // 3 x held_cap int64
@@ -183,6 +188,7 @@ int cuda_error(fgbd_ctx* ctx, cudaError_t e, const char* where);
   } while (0)
 
 int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64);
+int require_point_rows(fgbd_ctx* ctx);
 // (N,3) colours (host or device) -> BUF_Y in the (N,4) layout
 int upload_colors(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev);
 // same, issued on the side stream; the main stream waits for it at ev_side
@@ -194,7 +200,9 @@ int ensure_w64(fgbd_ctx* ctx, int64_t n);
 // ---- graph construction (graph.cu) --------------------------------------
 // Builds pc, sorts the 3 scan lines, writes cand/ell/meta, reduces sigma_g.
 // coords64 already on device.  No host sync.
-int launch_graph(fgbd_ctx* ctx, int64_t n, int bits);
+// reorder: store rows in scan-line-1 order (ctx->rowid / ctx->pos) -- the
+// denoise path; stage-API graphs keep rows in point order
+int launch_graph(fgbd_ctx* ctx, int64_t n, int bits, bool reorder = false);
 // Converts the ell payload (squared distances) into Gaussian weights.
 int launch_weights(fgbd_ctx* ctx, int64_t n, int bits, int w64);
 // Stand-alone stable argsort of 64-bit keys (radix_argsort).

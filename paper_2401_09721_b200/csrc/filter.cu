@@ -62,21 +62,26 @@ __device__ __forceinline__ double criterion(const double sy[3], const double sx[
 // layout conversion
 // ---------------------------------------------------------------------------
 
+// row k of the signal holds point rowid[k] (identity when rowid is null)
 __global__ void __launch_bounds__(kBlock) k_expand(const double* __restrict__ src, int64_t n,
-                                                   double4* __restrict__ dst) {
+                                                   double4* __restrict__ dst,
+                                                   const uint32_t* __restrict__ rowid) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    st_row(dst + i, make_double4(src[3 * i], src[3 * i + 1], src[3 * i + 2], 0.0));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t p = rowid ? (int64_t)rowid[i] : i;
+    st_row(dst + i, make_double4(src[3 * p], src[3 * p + 1], src[3 * p + 2], 0.0));
+  }
 }
 
 template <bool CLIP>
 __global__ void __launch_bounds__(kBlock) k_compact(double* const* bufs, const Ctl* ctl,
                                                     const double4* src, int64_t n,
-                                                    double* __restrict__ dst) {
+                                                    double* __restrict__ dst,
+                                                    const int* __restrict__ pos) {
   const double4* s = src ? src : reinterpret_cast<const double4*>(bufs[ctl->best_buf]);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const double4 v = ld_row(s + i);
+    const double4 v = ld_row(s + (pos ? (int64_t)pos[i] : i));  // point i lives in row pos[i]
     if (CLIP) {
       dst[3 * i] = fmin(fmax(v.x, 0.0), 255.0);
       dst[3 * i + 1] = fmin(fmax(v.y, 0.0), 255.0);
@@ -197,6 +202,7 @@ struct StepArgs {
   int fixed_steps;  // cached path: number of steps (Y -> A/B ping-pong)
   int64_t chunk;    // persistent kernels: rows per block (contiguous), 0 = grid-stride
   int halo;         // TMA-staged sweep: window rows either side of a row tile
+  const uint32_t* rowid;  // row -> point when rows are in scan-line-1 order (else null)
   int exp;          // timing experiments only (FGBD_LF_EXP): 1 no sums, 2 no reduction, 4 two-buffer rotation
   unsigned long long* flags;  // P2P: per-block "step published" words (monotone across launches)
   unsigned long long base;    // P2P: this launch's flag base (published value = base + step)
@@ -266,13 +272,17 @@ __device__ __forceinline__ void load_row_slots(const StepArgs& a, int64_t i, uin
   if (WM != W_STORED) {
     using K = typename std::conditional<WM == W_COORDS32, uint32_t, unsigned long long>::type;
     const K* pc = reinterpret_cast<const K*>(a.pc);
-    const K own = pc[i];
+    const K own = pc[a.rowid ? a.rowid[i] : i];
     K pj[kSlots];
 #pragma unroll
-    for (int s = 0; s < kSlots; ++s) pj[s] = pc[nb[s]];
+    for (int s = 0; s < kSlots; ++s) {
+      const int j = ell_j(nb[s]);
+      pj[s] = pc[a.rowid ? a.rowid[j] : j];
+    }
 #pragma unroll
     for (int s = 0; s < kSlots; ++s)
-      w[s] = nb[s] != (int)i ? __expf((float)sqlen(own, pj[s], a.bits) * neg_inv_sg2) : 0.0f;
+      w[s] = ell_j(nb[s]) != (int)i ? __expf((float)sqlen(own, pj[s], a.bits) * neg_inv_sg2)
+                                    : 0.0f;
   }
 }
 
@@ -290,15 +300,18 @@ __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const
 #pragma unroll
   for (int s = 0; s < kSlots; ++s)
 #if FGBD_LF_SIGHINT
-    g[s] = ld_row_hint(in + nb[s], pol_keep);
+    g[s] = ld_row_hint(in + ell_j(nb[s]), pol_keep);
 #else
-    g[s] = ld_row(in + nb[s]);
+    g[s] = ld_row(in + ell_j(nb[s]));
 #endif
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
+    // the ELL word's bit 31 says whether the neighbour's ORIGINAL index is
+    // below this row's point; padding (own row, w = 0) adds +0.0 to hi
     const double w = (double)wf[s];
-    lo = __dadd_rn(lo, nb[s] < (int)i ? w : 0.0);
-    hi = __dadd_rn(hi, nb[s] > (int)i ? w : 0.0);
+    const bool below = ell_below(nb[s]);
+    lo = __dadd_rn(lo, below ? w : 0.0);
+    hi = __dadd_rn(hi, below ? 0.0 : w);
     acc0 = __dadd_rn(acc0, __dmul_rn(w, g[s].x));
     acc1 = __dadd_rn(acc1, __dmul_rn(w, g[s].y));
     acc2 = __dadd_rn(acc2, __dmul_rn(w, g[s].z));
@@ -306,12 +319,12 @@ __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const
 #else
 #pragma unroll
   for (int s = 0; s < kSlots; ++s)
-    g[s] = (wf[s] != 0.0f) ? ld_row_hint(in + nb[s], pol_keep) : make_double4(0, 0, 0, 0);
+    g[s] = (wf[s] != 0.0f) ? ld_row_hint(in + ell_j(nb[s]), pol_keep) : make_double4(0, 0, 0, 0);
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
     const double w = (double)wf[s];
-    if (nb[s] < (int)i) lo = __dadd_rn(lo, w);
-    else if (nb[s] > (int)i) hi = __dadd_rn(hi, w);
+    if (ell_below(nb[s])) lo = __dadd_rn(lo, w);
+    else if (ell_j(nb[s]) != (int)i) hi = __dadd_rn(hi, w);
     if (wf[s] != 0.0f) {
       acc0 = __dadd_rn(acc0, __dmul_rn(w, g[s].x));
       acc1 = __dadd_rn(acc1, __dmul_rn(w, g[s].y));
@@ -341,10 +354,10 @@ __device__ __forceinline__ double4 row_w64(const StepArgs& a, const double4* in,
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
-    if (nb[s] < (int)i) lo = __dadd_rn(lo, w[s]);
-    else if (nb[s] > (int)i) hi = __dadd_rn(hi, w[s]);
+    if (ell_below(nb[s])) lo = __dadd_rn(lo, w[s]);
+    else if (ell_j(nb[s]) != (int)i) hi = __dadd_rn(hi, w[s]);
     if (w[s] != 0.0) {
-      const double4 g = ld_row(in + nb[s]);
+      const double4 g = ld_row(in + ell_j(nb[s]));
       acc0 = __dadd_rn(acc0, __dmul_rn(w[s], g.x));
       acc1 = __dadd_rn(acc1, __dmul_rn(w[s], g.y));
       acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g.z));
@@ -536,14 +549,17 @@ __device__ __forceinline__ void sweep_tma(const StepArgs& a, const double4* in, 
       const int4* E = reinterpret_cast<const int4*>(base + kWinRows * 32);
       int nb[kSlots];
       float wf[kSlots];
+      int raw[kSlots];
 #pragma unroll
       for (int p = 0; p < 3; ++p) {
         const int4 pr = E[p * kTile + threadIdx.x];
-        nb[2 * p] = pr.x;
+        raw[2 * p] = pr.x;
         wf[2 * p] = __int_as_float(pr.y);
-        nb[2 * p + 1] = pr.z;
+        raw[2 * p + 1] = pr.z;
         wf[2 * p + 1] = __int_as_float(pr.w);
       }
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) nb[s] = ell_j(raw[s]);
       // far neighbours first (global), then the window (shared)
       double4 g[kSlots];
 #pragma unroll
@@ -562,8 +578,8 @@ __device__ __forceinline__ void sweep_tma(const StepArgs& a, const double4* in, 
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {
         const double w = (double)wf[s];
-        if (nb[s] < (int)i) dlo = __dadd_rn(dlo, w);
-        else if (nb[s] > (int)i) dhi = __dadd_rn(dhi, w);
+        if (ell_below(raw[s])) dlo = __dadd_rn(dlo, w);
+        else if (nb[s] != (int)i) dhi = __dadd_rn(dhi, w);
         if (wf[s] != 0.0f) {
           acc0 = __dadd_rn(acc0, __dmul_rn(w, g[s].x));
           acc1 = __dadd_rn(acc1, __dmul_rn(w, g[s].y));
@@ -650,7 +666,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {
-        const int j = __ldg(a.E.nbr + eslot(s, a.n, i));
+        const int j = ell_j(__ldg(a.E.nbr + eslot(s, a.n, i)));
         mn = min(mn, j);
         mx = max(mx, j);
       }
@@ -909,19 +925,21 @@ static int fill_grid(fgbd_ctx* ctx, int64_t n) {
 }
 
 int launch_expand(fgbd_ctx* ctx, const double* d_src, int64_t n, int buf, cudaStream_t s) {
-  k_expand<<<fill_grid(ctx, n), kBlock, 0, s>>>(d_src, n, (double4*)ctx->buf[buf]);
+  k_expand<<<fill_grid(ctx, n), kBlock, 0, s>>>(d_src, n, (double4*)ctx->buf[buf],
+                                                ctx->g_reordered ? ctx->rowid : nullptr);
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
 }
 
 int launch_compact(fgbd_ctx* ctx, int64_t n, int src_buf, double* d_dst, int clip) {
   const double4* src = src_buf >= 0 ? (const double4*)ctx->buf[src_buf] : nullptr;
+  const int* pos = ctx->g_reordered ? ctx->pos : nullptr;
   if (clip)
     k_compact<true><<<fill_grid(ctx, n), kBlock, 0, ctx->stream>>>(ctx->d_bufs, ctx->ctl, src, n,
-                                                                   d_dst);
+                                                                   d_dst, pos);
   else
     k_compact<false><<<fill_grid(ctx, n), kBlock, 0, ctx->stream>>>(ctx->d_bufs, ctx->ctl, src, n,
-                                                                    d_dst);
+                                                                    d_dst, pos);
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
 }
@@ -958,6 +976,7 @@ static StepArgs step_args(fgbd_ctx* ctx, int64_t n) {
   a.n = n;
   a.part = ctx->partials;
   a.ctl = ctx->ctl;
+  a.rowid = ctx->g_reordered ? ctx->rowid : nullptr;
   return a;
 }
 

@@ -298,7 +298,8 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
 __global__ void __launch_bounds__(kBlock) k_neighbors(const uint32_t* __restrict__ p0,
                                                      const uint32_t* __restrict__ p1,
                                                      const uint32_t* __restrict__ p2,
-                                                     int64_t n, int2* __restrict__ cand) {
+                                                     int64_t n, int2* __restrict__ cand,
+                                                     int* __restrict__ pos) {
   const int line = blockIdx.y;
   const uint32_t* perm = line == 0 ? p0 : (line == 1 ? p1 : p2);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(kBlock) k_neighbors(const uint32_t* __restrict
     const int prev = k > 0 ? (int)perm[k - 1] : -1;
     const int next = k + 1 < n ? (int)perm[k + 1] : -1;
     cand[line * n + u] = make_int2(prev, next);
+    if (line == 0 && pos) pos[u] = (int)k;  // row of point u = its scan-line-1 rank
   }
 }
 
@@ -334,7 +336,8 @@ __device__ __forceinline__ void sort6(unsigned (&c)[6]) {
 template <typename K, bool BIG>
 __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
                                                  const K* __restrict__ pc, int64_t n, int b,
-                                                 EllRef ell,
+                                                 const int* __restrict__ pos,
+                                                 const uint32_t* __restrict__ rowid, EllRef ell,
                                                  uint32_t* __restrict__ meta,
                                                  double* __restrict__ partials,
                                                  Ctl* __restrict__ ctl) {
@@ -343,7 +346,9 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
   double sg_sum = 0.0, e_cnt = 0.0;
   int maxdeg = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  // walk the ROWS (coalesced ELL / meta writes); row rr holds point i
+  for (int64_t rr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rr < n; rr += stride) {
+    const int64_t i = rowid ? (int64_t)rowid[rr] : rr;
     unsigned c[6];
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
@@ -387,13 +392,53 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
         r += (t < deg) && (sq[t] < sq[s] || (sq[t] == sq[s] && t < s));
       if (s < deg) order |= (uint32_t)s << (3 * r);
     }
+    // the row of point i (its line-1 rank when rows are reordered) and its
+    // neighbours' rows
+    const int64_t r = rr;
+    int word[6];
+    unsigned slot_of[6];  // ELL slot that receives candidate slot s
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
-      const bool ok = s < deg;
-      ell.nbr[eslot(s, n, i)] = ok ? (int)c[s] : (int)i;
-      ell.pay[eslot(s, n, i)] = (ok && !BIG) ? (uint32_t)sq[s] : 0u;
+      int w = (int)r;  // padding: (own row, 0)
+      if (s < deg) {
+        const int jr = pos ? pos[c[s]] : (int)c[s];
+        w = jr | ((int64_t)c[s] < i ? kBelowBit : 0);
+      }
+      word[s] = w;
+      slot_of[s] = s;
     }
-    meta[i] = (uint32_t)deg | (order << 3);
+    if (pos) {
+      // reordered rows: store the real slots by ascending neighbour ROW, so
+      // the lanes of a warp (consecutive rows) gather slot t from nearby
+      // rows -- for point-order rows this is the index order already
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        int rk = 0;
+#pragma unroll
+        for (int t = 0; t < 6; ++t)
+          rk += (t < deg) && (ell_j(word[t]) < ell_j(word[s]) ||
+                              (ell_j(word[t]) == ell_j(word[s]) && t < s));
+        if (s < deg) slot_of[s] = (unsigned)rk;
+      }
+      // the patch order names slots: renumber it
+      uint32_t o2 = 0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const unsigned sl = (order >> (3 * k)) & 7u;
+        unsigned ns = 0;
+#pragma unroll
+        for (int s = 0; s < 6; ++s) ns = (sl == (unsigned)s) ? slot_of[s] : ns;
+        if (k < deg) o2 |= ns << (3 * k);
+      }
+      order = o2;
+    }
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int t = (int)slot_of[s];
+      ell.nbr[eslot(t, n, r)] = word[s];
+      ell.pay[eslot(t, n, r)] = (s < deg && !BIG) ? (uint32_t)sq[s] : 0u;
+    }
+    meta[r] = (uint32_t)deg | (order << 3);
     maxdeg = max(maxdeg, deg);
   }
   // block reduce (sum, count) and the max degree
@@ -427,22 +472,24 @@ template <typename K, bool BIG, bool W64>
 __global__ void __launch_bounds__(kBlock) k_weights(EllRef ell,
                                                     double* __restrict__ w64,
                                                     const K* __restrict__ pc, int64_t n,
-                                                    int b, const Ctl* __restrict__ ctl) {
+                                                    int b, const uint32_t* __restrict__ rowid,
+                                                    const Ctl* __restrict__ ctl) {
   const double sg = ctl->sigma_g;
   const double sg2 = sg * sg;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     long long xi = 0, yi = 0, zi = 0;
-    if (BIG) unpack(pc[i], b, &xi, &yi, &zi);
+    if (BIG) unpack(pc[rowid ? rowid[i] : i], b, &xi, &yi, &zi);
 #pragma unroll
     for (int s = 0; s < kSlots; ++s) {
       int2 sl = make_int2(ell.nbr[eslot(s, n, i)], (int)ell.pay[eslot(s, n, i)]);
       double w = 0.0;
-      if (sl.x != (int)i) {
+      const int j = ell_j(sl.x);
+      if (j != (int)i) {
         unsigned long long sq;
         if (BIG) {
           long long xj, yj, zj;
-          unpack(pc[sl.x], b, &xj, &yj, &zj);
+          unpack(pc[rowid ? rowid[j] : j], b, &xj, &yj, &zj);
           const long long dx = xi - xj, dy = yi - yj, dz = zi - zj;
           sq = (unsigned long long)(dx * dx + dy * dy + dz * dz);
         } else {
@@ -467,7 +514,7 @@ __global__ void k_degrees(const uint32_t* __restrict__ meta, const int* __restri
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int dg = (int)(meta[i] & 7u);
     int up = 0;
-    for (int s = 0; s < dg; ++s) up += (ell[eslot(s, n, i)] > (int)i);
+    for (int s = 0; s < dg; ++s) up += (ell_j(ell[eslot(s, n, i)]) > (int)i);
     deg[i] = dg;
     updeg[i] = up;
   }
@@ -545,7 +592,7 @@ __global__ void k_export(const uint32_t* __restrict__ meta, const int* __restric
     int nlow = 0;
     double lo = 0.0, hi = 0.0;
     for (int s = 0; s < dg; ++s) {
-      const int j = ell[eslot(s, n, i)];
+      const int j = ell_j(ell[eslot(s, n, i)]);
       long long xj, yj, zj;
       unpack(pc[j], b, &xj, &yj, &zj);
       const long long dx = xi - xj, dy = yi - yj, dz = zi - zj;
@@ -564,7 +611,7 @@ __global__ void k_export(const uint32_t* __restrict__ meta, const int* __restric
         const int dj = (int)(meta[j] & 7u);
         int cnt = 0;
         for (int t = 0; t < dj; ++t) {
-          const int v = ell[eslot(t, n, j)];
+          const int v = ell_j(ell[eslot(t, n, j)]);
           cnt += (v > j) && (v < (int)i);
         }
         eid = eoff[j] + cnt;
@@ -659,23 +706,27 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
 }
 
 template <typename K>
-static int graph_impl(fgbd_ctx* ctx, int64_t n, int b) {
+static int graph_impl(fgbd_ctx* ctx, int64_t n, int b, bool reorder) {
   const int passes = (3 * b + 7) / 8;
   int rc = run_sort<K, true>(ctx, n, b, 3, passes, nullptr);
   if (rc) return rc;
+  // rows in scan-line-1 order: row k holds the point of line-1 rank k
+  ctx->rowid = reorder ? ctx->perm[0] : nullptr;
+  if (reorder) FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_perm, ctx->stream));
+  int* pos = reorder ? ctx->pos : nullptr;
   {
     dim3 grid(grid_for(n, 1 << 20), 3);
     k_neighbors<<<grid, kBlock, 0, ctx->stream>>>(ctx->perm[0], ctx->perm[1], ctx->perm[2], n,
-                                                  ctx->cand);
+                                                  ctx->cand, pos);
     FGBD_LAUNCH(ctx);
   }
   const int grid = grid_for(n, kRowsGrid);
   if (b > 15) {
-    k_rows<K, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b,
+    k_rows<K, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b, pos, ctx->rowid,
                                                       EllRef{ctx->nbr, ctx->pay}, ctx->meta, ctx->partials,
                                                       ctx->ctl);
   } else {
-    k_rows<K, false><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b,
+    k_rows<K, false><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b, pos, ctx->rowid,
                                                        EllRef{ctx->nbr, ctx->pay}, ctx->meta, ctx->partials,
                                                        ctx->ctl);
   }
@@ -683,10 +734,11 @@ static int graph_impl(fgbd_ctx* ctx, int64_t n, int b) {
   return FGBD_OK;
 }
 
-int launch_graph(fgbd_ctx* ctx, int64_t n, int bits) {
-  int rc = (3 * bits <= 32) ? graph_impl<uint32_t>(ctx, n, bits)
-                            : graph_impl<unsigned long long>(ctx, n, bits);
+int launch_graph(fgbd_ctx* ctx, int64_t n, int bits, bool reorder) {
+  int rc = (3 * bits <= 32) ? graph_impl<uint32_t>(ctx, n, bits, reorder)
+                            : graph_impl<unsigned long long>(ctx, n, bits, reorder);
   if (rc) return rc;
+  ctx->g_reordered = reorder ? 1 : 0;
   ctx->g_n = n;
   ctx->g_bits = bits;
   ctx->g_have_weights = 0;
@@ -701,14 +753,14 @@ static int weights_impl(fgbd_ctx* ctx, int64_t n, int b, int w64) {
   const K* pc = (const K*)ctx->pc;
   if (b > 15) {
     if (w64)
-      k_weights<K, true, true><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->ctl);
+      k_weights<K, true, true><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->rowid, ctx->ctl);
     else
-      k_weights<K, true, false><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->ctl);
+      k_weights<K, true, false><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->rowid, ctx->ctl);
   } else {
     if (w64)
-      k_weights<K, false, true><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->ctl);
+      k_weights<K, false, true><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->rowid, ctx->ctl);
     else
-      k_weights<K, false, false><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->ctl);
+      k_weights<K, false, false><<<grid, kBlock, 0, ctx->stream>>>(EllRef{ctx->nbr, ctx->pay}, ctx->w64, pc, n, b, ctx->rowid, ctx->ctl);
   }
   FGBD_LAUNCH(ctx);
   return FGBD_OK;

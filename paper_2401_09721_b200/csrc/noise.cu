@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict
     if (valid) {
       mt = meta[i];
 #pragma unroll
-      for (int s = 0; s < kSlots; ++s) nb[s] = ell[eslot(s, n, i)];
+      for (int s = 0; s < kSlots; ++s) nb[s] = ell_j(ell[eslot(s, n, i)]);
       a[0] = colors[4 * i + c];
     }
     const int deg = (int)(mt & 7u);
@@ -188,11 +188,12 @@ __global__ void __launch_bounds__(kNe2Warps * 32, 6) k_noise2(const uint32_t* __
 #pragma unroll
       for (int s = 0; s < kSlots; s += 2) {
         int4 pr = *reinterpret_cast<const int4*>(ell.nbr + eslot(s, n, i));
-        nb[s] = pr.x;
-        nb[s + 1] = pr.z;
+        nb[s] = ell_j(pr.x);
+        nb[s + 1] = ell_j(pr.z);
         if (WEIGHTS) {
-          const double w0 = pr.x != (int)i ? exp(__ddiv_rn(-(double)(uint32_t)pr.y, sg2)) : 0.0;
-          const double w1 = pr.z != (int)i ? exp(__ddiv_rn(-(double)(uint32_t)pr.w, sg2)) : 0.0;
+          const double w0 = nb[s] != (int)i ? exp(__ddiv_rn(-(double)(uint32_t)pr.y, sg2)) : 0.0;
+          const double w1 =
+              nb[s + 1] != (int)i ? exp(__ddiv_rn(-(double)(uint32_t)pr.w, sg2)) : 0.0;
           pr.y = __float_as_int((float)w0);
           pr.w = __float_as_int((float)w1);
           *reinterpret_cast<int4*>(ell.nbr + eslot(s, n, i)) = pr;

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
       for (int s = 0; s < kSlots; s += 2) {
         const int4 pr =
             ld_pair_hint(reinterpret_cast<const int2*>(a.E.nbr + eslot(s, a.n, i)), pol_stream);
-        nb[s] = pr.x;
+        nb[s] = pr.x;  // row | below-flag (bit 31)
         w[s] = __int_as_float(pr.y);
         nb[s + 1] = pr.z;
         w[s + 1] = __int_as_float(pr.w);
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {
         if (w[s] != 0.0f) {
-          const int64_t j = nb[s];
+          const int64_t j = ell_j(nb[s]);
           const int o = (j >= lo && j < hi) ? r : owner_of(a, j);  // halo: owner's buffer
           gv[s] = ld_row(a.bufs[o][ib] + j);
         } else {
@@ -181,8 +181,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
 #pragma unroll
       for (int s = 0; s < kSlots; ++s) {
         const double ws = (double)w[s];
-        if (nb[s] < (int)i) dlo = __dadd_rn(dlo, ws);
-        else if (nb[s] > (int)i) dhi = __dadd_rn(dhi, ws);
+        // (sum over original j > i) + (sum over j < i); padding has w = 0
+        if (ell_below(nb[s])) dlo = __dadd_rn(dlo, ws);
+        else if (ell_j(nb[s]) != (int)i) dhi = __dadd_rn(dhi, ws);
         if (w[s] != 0.0f) {
           acc0 = __dadd_rn(acc0, __dmul_rn(ws, gv[s].x));
           acc1 = __dadd_rn(acc1, __dmul_rn(ws, gv[s].y));
@@ -270,10 +271,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
 // Assemble the full (N,3) clipped output from every rank's best buffer
 // (peer loads for foreign rows).
 __global__ void __launch_bounds__(kBlock) k_slab_gather(SlabArgs a, int best_b,
-                                                        double* __restrict__ dst, int clip) {
+                                                        double* __restrict__ dst, int clip,
+                                                        const int* __restrict__ pos) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
-    const double4 v = ld_row(a.bufs[owner_of(a, i)][best_b] + i);
+    const int64_t r = pos ? (int64_t)pos[i] : i;  // point i lives in row r
+    const double4 v = ld_row(a.bufs[owner_of(a, r)][best_b] + r);
     if (clip) {
       dst[3 * i] = fmin(fmax(v.x, 0.0), 255.0);
       dst[3 * i + 1] = fmin(fmax(v.y, 0.0), 255.0);
@@ -400,8 +403,8 @@ int launch_slab(fgbd_ctx* ctx, fgbd_slab* s, int64_t n, int select, int fixed_st
   FGBD_CUDA(ctx, cudaMemcpyAsync(&ctx->ctl_host->best_buf, &ctx->ctl->best_buf, sizeof(int),
                                  cudaMemcpyDeviceToHost, ctx->stream));
   FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  k_slab_gather<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(a, ctx->ctl_host->best_buf, d_out,
-                                                             1);
+  k_slab_gather<<<ctx->num_sms * 4, kBlock, 0, ctx->stream>>>(
+      a, ctx->ctl_host->best_buf, d_out, 1, ctx->g_reordered ? ctx->pos : nullptr);
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
 }

@@ -34,7 +34,7 @@ __global__ void k_extract(const uint32_t* __restrict__ meta, const int* __restri
     for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D] = colors[4 * i + c];
     for (int r = 1; r < D; ++r) {
       const int s = (int)((mt >> (3 + 3 * (r - 1))) & 7u);
-      const int64_t j = ell[eslot(s, n, i)];
+      const int64_t j = ell_j(ell[eslot(s, n, i)]);
       for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D + r] = colors[4 * j + c];
     }
   }
@@ -80,6 +80,7 @@ int32_t fgbd_extract_patches(fgbd_ctx* ctx, const double* colors, int32_t D,
   cudaSetDevice(ctx->device);
   ctx->err.clear();
   if (ctx->g_n < 0) return set_error(ctx, FGBD_E_GRAPH, "no graph held by this context");
+  if (int e = require_point_rows(ctx)) return e;
   if (D < 2) return set_error(ctx, FGBD_E_NOISE, "patch_size must be >= 2, got " + std::to_string(D));
   const int64_t n = ctx->g_n;
   int maxdeg = 0;

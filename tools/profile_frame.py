@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--frames", type=int, default=3)
     ap.add_argument("--cached", type=int, default=-1)
     ap.add_argument("--no-early-exit", action="store_true")
+    ap.add_argument("--order", default="asis", choices=["asis", "shuffle", "morton", "line1"],
+                    help="permute the points before upload (locality experiments)")
     a = ap.parse_args()
     import torch
 
@@ -34,6 +36,22 @@ def main():
 
     clean, _ = fb.generate_cloud(a.kind, a.n, seed=0)
     noisy = fb.add_gaussian_noise(clean, a.sigma, seed=1)
+    if a.order != "asis":
+        g = np.array(noisy.coords)
+        if a.order == "shuffle":
+            perm = np.random.default_rng(7).permutation(a.n)
+        elif a.order == "line1":
+            perm = np.lexsort((g[:, 0], g[:, 1], g[:, 2]))
+        else:  # morton (z-order) of the voxel coordinates
+            def spread(v):
+                v = v.astype(np.uint64) & np.uint64(0x1FFFFF)
+                out = np.zeros_like(v)
+                for bit in range(21):
+                    out |= ((v >> np.uint64(bit)) & np.uint64(1)) << np.uint64(3 * bit)
+                return out
+            code = spread(g[:, 0]) | (spread(g[:, 1]) << np.uint64(1)) | (spread(g[:, 2]) << np.uint64(2))
+            perm = np.argsort(code, kind="stable")
+        noisy = fb.PointCloud(g[perm], np.array(noisy.colors)[perm], noisy.bit_depth)
     ctx = nat.context()
     dc = torch.from_numpy(np.array(noisy.coords)).cuda()
     dy = torch.from_numpy(np.array(noisy.colors)).cuda()
