@@ -321,3 +321,32 @@ def test_slab_partition_full_size(gpu_ready):
         assert rb.selected_q == ra.selected_q == rec["report"]["selected_q"]
         assert rb.device["steps"] == rec["steps"]
         assert np.array_equal(a.colors, b.colors)
+
+
+# ---------------------------------------------------------------------------
+# input point order: the device stores rows in scan-line-1 order internally;
+# any input order must give the reference's (= oracle's) answer for that order
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("order", ["shuffle", "reverse", "morton"])
+def test_input_order_matches_oracle(gpu_ready, order):
+    clean, _ = fb.generate_cloud("ramp", 20_000, seed=0)
+    noisy = fb.add_gaussian_noise(clean, 15.0, seed=2)
+    g = np.array(noisy.coords)
+    if order == "shuffle":
+        perm = np.random.default_rng(5).permutation(g.shape[0])
+    elif order == "reverse":
+        perm = np.arange(g.shape[0])[::-1]
+    else:
+        key = np.zeros(g.shape[0], np.int64)
+        for bit in range(8):
+            for a in range(3):
+                key |= ((g[:, a] >> bit) & 1) << (3 * bit + a)
+        perm = np.argsort(key, kind="stable")
+    pc = fb.PointCloud(g[perm], np.array(noisy.colors)[perm], noisy.bit_depth)
+    out, rep = fb.denoise(pc)
+    ref = O.denoise(pc.coords, pc.colors, pc.bit_depth)
+    assert rep.selected_q == ref.selected_q
+    assert rep.device["steps"] == ref.steps
+    assert rep.sigma_est == pytest.approx(ref.sigma_est, rel=SIGMA_RTOL)
+    assert np.max(np.abs(out.colors - ref.colors)) <= COLOR_ATOL
