@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
   }
   __syncthreads();
   const int64_t lo = a.lo[r], hi = a.lo[r + 1];
-  const int64_t stride = (int64_t)a.bpg * blockDim.x;
+  const int64_t chunk = ((hi - lo + a.bpg - 1) / a.bpg + blockDim.x - 1) / blockDim.x * blockDim.x;
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
   unsigned int* gbar = a.gbar + 2 * g;
   while (!s_st.stop) {
@@ -153,56 +153,73 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
     if (ob == ib || ob == bb) ob = BUF_Y;
     double4* out = a.bufs[r][ob];
     double sx[3] = {0.0, 0.0, 0.0};
-    for (int64_t i = lo + (int64_t)lb * blockDim.x + threadIdx.x; i < hi; i += stride) {
-      int nb[kSlots];
-      float w[kSlots];
+    {
+      // this block's contiguous share of the rank's rows, next row's slots
+      // prefetched; gathers are branch-free (padding = own row, w = 0) and
+      // only rows outside [lo, hi) look up their owner's (peer) buffer
+      const double4* own_in = a.bufs[r][ib];
+      int64_t i = lo + (int64_t)lb * chunk + threadIdx.x;
+      const int64_t end = min(hi, lo + (int64_t)(lb + 1) * chunk);
+      int nbn[kSlots];
+      float wn[kSlots];
+      auto load_slots = [&](int64_t row, int (&nb)[kSlots], float (&w)[kSlots]) {
 #pragma unroll
-      for (int s = 0; s < kSlots; s += 2) {
-        const int4 pr =
-            ld_pair_hint(reinterpret_cast<const int2*>(a.E.nbr + eslot(s, a.n, i)), pol_stream);
-        nb[s] = pr.x;  // row | below-flag (bit 31)
-        w[s] = __int_as_float(pr.y);
-        nb[s + 1] = pr.z;
-        w[s + 1] = __int_as_float(pr.w);
-      }
-      const double4 f = ld_row_hint(a.bufs[r][ib] + i, pol_keep);
-      double4 gv[kSlots];
-#pragma unroll
-      for (int s = 0; s < kSlots; ++s) {
-        if (w[s] != 0.0f) {
-          const int64_t j = ell_j(nb[s]);
-          const int o = (j >= lo && j < hi) ? r : owner_of(a, j);  // halo: owner's buffer
-          gv[s] = ld_row(a.bufs[o][ib] + j);
-        } else {
-          gv[s] = make_double4(0, 0, 0, 0);
+        for (int s = 0; s < kSlots; s += 2) {
+          const int4 pr =
+              ld_pair_hint(reinterpret_cast<const int2*>(a.E.nbr + eslot(s, a.n, row)), pol_stream);
+          nb[s] = pr.x;  // row | below-flag (bit 31)
+          w[s] = __int_as_float(pr.y);
+          nb[s + 1] = pr.z;
+          w[s + 1] = __int_as_float(pr.w);
         }
-      }
-      double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, dlo = 0.0, dhi = 0.0;
+      };
+      if (i < end) load_slots(i, nbn, wn);
+      while (i < end) {
+        int nb[kSlots];
+        float w[kSlots];
 #pragma unroll
-      for (int s = 0; s < kSlots; ++s) {
-        const double ws = (double)w[s];
-        // (sum over original j > i) + (sum over j < i); padding has w = 0
-        if (ell_below(nb[s])) dlo = __dadd_rn(dlo, ws);
-        else if (ell_j(nb[s]) != (int)i) dhi = __dadd_rn(dhi, ws);
-        if (w[s] != 0.0f) {
+        for (int s = 0; s < kSlots; ++s) {
+          nb[s] = nbn[s];
+          w[s] = wn[s];
+        }
+        const int64_t inext = i + blockDim.x;
+        if (inext < end) load_slots(inext, nbn, wn);
+        const double4 f = ld_row_hint(own_in + i, pol_keep);
+        double4 gv[kSlots];
+#pragma unroll
+        for (int s = 0; s < kSlots; ++s) {
+          const int64_t j = ell_j(nb[s]);
+          const double4* src =
+              (j >= lo && j < hi) ? own_in : a.bufs[owner_of(a, j)][ib];  // halo: peer memory
+          gv[s] = ld_row_hint(src + j, pol_keep);
+        }
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, dlo = 0.0, dhi = 0.0;
+#pragma unroll
+        for (int s = 0; s < kSlots; ++s) {
+          // (sum over original j > i) + (sum over j < i); padding adds +0.0
+          const double ws = (double)w[s];
+          const bool below = ell_below(nb[s]);
+          dlo = __dadd_rn(dlo, below ? ws : 0.0);
+          dhi = __dadd_rn(dhi, below ? 0.0 : ws);
           acc0 = __dadd_rn(acc0, __dmul_rn(ws, gv[s].x));
           acc1 = __dadd_rn(acc1, __dmul_rn(ws, gv[s].y));
           acc2 = __dadd_rn(acc2, __dmul_rn(ws, gv[s].z));
         }
-      }
-      const double d = __dadd_rn(dhi, dlo);
-      double4 o = f;
-      if (d != 0.0) {
-        const double d2 = __dmul_rn(2.0, d);
-        o = make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
-                         __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
-                         __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
-      }
-      st_row_hint(out + i, o, pol_keep);
-      if (a.select && (s_mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
-        sx[0] = fma(o.x, o.x, sx[0]);
-        sx[1] = fma(o.y, o.y, sx[1]);
-        sx[2] = fma(o.z, o.z, sx[2]);
+        const double d = __dadd_rn(dhi, dlo);
+        double4 o = f;
+        if (d != 0.0) {
+          const double d2 = __dmul_rn(2.0, d);
+          o = make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
+                           __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
+                           __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
+        }
+        st_row_hint(out + i, o, pol_keep);
+        if (a.select && (s_mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+          sx[0] = fma(o.x, o.x, sx[0]);
+          sx[1] = fma(o.y, o.y, sx[1]);
+          sx[2] = fma(o.z, o.z, sx[2]);
+        }
+        i = inext;
       }
     }
     block_sum<3>(sx, s_red);
