@@ -253,3 +253,18 @@ def test_oracle_ell_step_equals_scipy_csr():
     d = g.weighted_degrees()[:, None]
     ref = (d * pc.colors + w @ pc.colors) / (2.0 * d)
     assert np.array_equal(O.EllOperator(g).step(pc.colors), ref)
+
+
+def test_ell_view_equals_csr_matvec():
+    """The oracle's step calls scipy's CSR matvec; the padded-row (ELL)
+    accumulation in slot order from 0.0 gives the same bits."""
+    rng = np.random.default_rng(4)
+    coords = rng.integers(0, 16, size=(3000, 3))
+    g = O.build_weighted_slg(coords, 4)
+    op = O.EllOperator(g)
+    f = rng.uniform(0, 255, size=(3000, 3))
+    idx, w = op.dense_rows()
+    acc = np.zeros_like(f)
+    for s in range(idx.shape[1]):
+        acc = acc + w[:, s, None] * f[idx[:, s]]
+    assert np.array_equal(acc, op.W @ f)
