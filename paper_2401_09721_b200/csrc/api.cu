@@ -439,7 +439,6 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_LF_SHAPE")) ctx->lf_shape = std::atoi(v) & 3;
   if (const char* v = std::getenv("FGBD_LF_CHUNK")) ctx->lf_chunk = std::atoi(v);
   if (const char* v = std::getenv("FGBD_REORDER")) ctx->reorder_rows = std::atoi(v);
-  if (const char* v = std::getenv("FGBD_LF_EXP")) ctx->lf_exp = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_HALO")) ctx->lf_halo = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (ensure_capacity(ctx, max_points > 0 ? max_points : 1, 0) != FGBD_OK) {

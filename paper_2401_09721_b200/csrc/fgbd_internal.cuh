@@ -122,7 +122,6 @@ struct fgbd_ctx {
   int coop_blocks[64] = {};      // co-resident grid of each persistent instantiation
   int lf_shape = 0;
   int lf_halo = 128;  // FGBD_LF_HALO: window rows either side of a TMA tile
-  int lf_exp = 0;    // FGBD_LF_EXP: timing experiments (filter.cu StepArgs::exp)
   int lf_chunk = 1;
   int reorder_rows = 1;  // FGBD_REORDER: denoise-path rows in scan-line-1 order  // FGBD_LF_CHUNK: contiguous row range per block (0 = grid-stride)             // persistent kernel block shape (FGBD_LF_SHAPE)
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)

@@ -203,7 +203,6 @@ struct StepArgs {
   int64_t chunk;    // persistent kernels: rows per block (contiguous), 0 = grid-stride
   int halo;         // TMA-staged sweep: window rows either side of a row tile
   const uint32_t* rowid;  // row -> point when rows are in scan-line-1 order (else null)
-  int exp;          // timing experiments only (FGBD_LF_EXP): 1 no sums, 2 no reduction, 4 two-buffer rotation
   unsigned long long* flags;  // P2P: per-block "step published" words (monotone across launches)
   unsigned long long base;    // P2P: this launch's flag base (published value = base + step)
 };
@@ -435,7 +434,7 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
     if (inext < end) load_row_slots<WM>(a, inext, pol_stream, neg_inv_sg2, nbn, wn);
     const double4 o = row_from_slots(nbc, wc, in, i, pol_keep);
     st_row_hint(out + i, o, pol_keep);
-    if (SUMS && !(a.exp & 1) && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+    if (SUMS && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
       sx[0] = fma(o.x, o.x, sx[0]);
       sx[1] = fma(o.y, o.y, sx[1]);
       sx[2] = fma(o.z, o.z, sx[2]);
@@ -708,7 +707,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       mbar_expect_tx(&s_pbar, bytes);
       bulk_g2s(s_part, a.part + (c & 1) * pstride, bytes, &s_pbar, policy_evict_last());
     }
-    const int ib = s_st.in_b, bb = (a.exp & 4) ? ib : s_st.best_b;
+    const int ib = s_st.in_b, bb = s_st.best_b;
     int ob = BUF_A;
     if (ob == ib || ob == bb) ob = BUF_B;
     if (ob == ib || ob == bb) ob = BUF_Y;
@@ -737,20 +736,18 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       }
       const double* part = a.part + (c & (kRing - 1)) * 3 * nb;
       double t[3] = {0.0, 0.0, 0.0};
-      if (!(a.exp & 2)) {
-        if (kBulkPart) {
-          mbar_wait(&s_pbar, pbar_uses & 1);
-          ++pbar_uses;
-          for (int b = threadIdx.x; b < nb; b += blockDim.x)
+      if (kBulkPart) {
+        mbar_wait(&s_pbar, pbar_uses & 1);
+        ++pbar_uses;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
 #pragma unroll
-            for (int k = 0; k < 3; ++k) t[k] += s_part[k * nb + b];
-        } else {
-          for (int b = threadIdx.x; b < nb; b += blockDim.x)
+          for (int k = 0; k < 3; ++k) t[k] += s_part[k * nb + b];
+      } else {
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
 #pragma unroll
-            for (int k = 0; k < 3; ++k) t[k] += __ldcg(&part[k * nb + b]);
-        }
-        block_sum<3>(t, s_red);
+          for (int k = 0; k < 3; ++k) t[k] += __ldcg(&part[k * nb + b]);
       }
+      block_sum<3>(t, s_red);
       if (threadIdx.x == 0) {
         const double crit = criterion(s_sy, t, s_inc, s_sv2, s_mode);
         s_st.out_b = s_st.in_b;  // x_c's buffer becomes the best if crit_c improves
@@ -1000,7 +997,6 @@ static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
                            kMaxCoopBlocks));
   a.chunk = (TMA || P2P || ctx->lf_chunk) ? ((a.n + grid - 1) / grid + BLK - 1) / BLK * BLK : 0;
   a.halo = std::min(ctx->lf_halo, kHaloMax);
-  a.exp = ctx->lf_exp;
   if (P2P) {
     if (!ctx->p2p_flags) {
       FGBD_CUDA(ctx, cudaMalloc(&ctx->p2p_flags, 8192 * sizeof(unsigned long long)));
