@@ -51,7 +51,7 @@ struct Ctl {
   unsigned long long n_edges;
   double sigma_g;
   int max_deg;
-  int err_flags;  // bit0: coordinate out of range
+  int err_flags;  // bit0: coordinate out of range, bit3: line-1 order is not the identity
   // noise estimation
   long long eligible;
   double gram[3][64];  // per-channel 8x8 Gram matrix of shifted patch rows

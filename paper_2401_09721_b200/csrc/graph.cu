@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kBlock) k_neighbors(const uint32_t* __restrict
                                                      const uint32_t* __restrict__ p1,
                                                      const uint32_t* __restrict__ p2,
                                                      int64_t n, int2* __restrict__ cand,
-                                                     int* __restrict__ pos) {
+                                                     int* __restrict__ pos, Ctl* __restrict__ ctl) {
   const int line = blockIdx.y;
   const uint32_t* perm = line == 0 ? p0 : (line == 1 ? p1 : p2);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -308,7 +308,13 @@ __global__ void __launch_bounds__(kBlock) k_neighbors(const uint32_t* __restrict
     const int prev = k > 0 ? (int)perm[k - 1] : -1;
     const int next = k + 1 < n ? (int)perm[k + 1] : -1;
     cand[line * n + u] = make_int2(prev, next);
-    if (line == 0 && pos) pos[u] = (int)k;  // row of point u = its scan-line-1 rank
+    if (line == 0 && pos) {
+      pos[u] = (int)k;  // row of point u = its scan-line-1 rank
+      // input already in line-1 order (raster scans): rows == points, and
+      // k_rows can skip the relabelling work
+      if (__any_sync(__activemask(), u != (int)k) && (threadIdx.x & 31) == 0)
+        atomicOr(&ctl->err_flags, 8);
+    }
   }
 }
 
@@ -346,6 +352,11 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
   double sg_sum = 0.0, e_cnt = 0.0;
   int maxdeg = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // rows differ from points only when the line-1 order is not the identity
+  if (pos && !(*(volatile const int*)&ctl->err_flags & 8)) {
+    pos = nullptr;
+    rowid = nullptr;
+  }
   // walk the ROWS (coalesced ELL / meta writes); row rr holds point i
   for (int64_t rr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rr < n; rr += stride) {
     const int64_t i = rowid ? (int64_t)rowid[rr] : rr;
@@ -717,7 +728,7 @@ static int graph_impl(fgbd_ctx* ctx, int64_t n, int b, bool reorder) {
   {
     dim3 grid(grid_for(n, 1 << 20), 3);
     k_neighbors<<<grid, kBlock, 0, ctx->stream>>>(ctx->perm[0], ctx->perm[1], ctx->perm[2], n,
-                                                  ctx->cand, pos);
+                                                  ctx->cand, pos, ctx->ctl);
     FGBD_LAUNCH(ctx);
   }
   const int grid = grid_for(n, kRowsGrid);
