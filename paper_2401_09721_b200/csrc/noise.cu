@@ -136,12 +136,12 @@ __device__ __forceinline__ double ch(const double4& v, int c) {
   return c == 0 ? v.x : (c == 1 ? v.y : v.z);
 }
 
-__device__ __forceinline__ double patch_std(const double4 (&v)[7], int c, int D) {
+__device__ __forceinline__ double patch_std(const double4 (&v)[7], int c, int D, double rD) {
   double sum = ch(v[0], c);
 #pragma unroll
   for (int k = 1; k < 7; ++k)
     if (k < D) sum = __dadd_rn(sum, ch(v[k], c));
-  const double mean = __ddiv_rn(sum, (double)D);
+  const double mean = div_rcp(sum, (double)D, rD);
   double var = 0.0;
 #pragma unroll
   for (int k = 0; k < 7; ++k) {
@@ -150,7 +150,7 @@ __device__ __forceinline__ double patch_std(const double4 (&v)[7], int c, int D)
       var = __dadd_rn(var, __dmul_rn(dv, dv));
     }
   }
-  return __dsqrt_rn(__ddiv_rn(var, (double)D));
+  return __dsqrt_rn(div_rcp(var, (double)D, rD));
 }
 
 template <bool WEIGHTS>
@@ -166,11 +166,15 @@ __global__ void __launch_bounds__(kNe2Warps * 32, 6) k_noise2(const uint32_t* __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* rows = s_rows[warp];
   double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-  double sg2 = 1.0;
+  double sg2 = 1.0, rsg2 = 0.0;
+  bool sg_rcp = false;
   if (WEIGHTS) {
     const double sg = ctl->sigma_g;
     sg2 = sg * sg;
+    sg_rcp = rcp_ok(sg2);
+    if (sg_rcp) rsg2 = __drcp_rn(sg2);
   }
+  const double rD = __drcp_rn((double)D), r3 = __drcp_rn(3.0);
   const int64_t nchunks = (n + 31) / 32;
   const int64_t wstride = (int64_t)gridDim.x * kNe2Warps;
   for (int64_t chk = (int64_t)blockIdx.x * kNe2Warps + warp; chk < nchunks; chk += wstride) {
@@ -191,9 +195,12 @@ __global__ void __launch_bounds__(kNe2Warps * 32, 6) k_noise2(const uint32_t* __
         nb[s] = ell_j(pr.x);
         nb[s + 1] = ell_j(pr.z);
         if (WEIGHTS) {
-          const double w0 = nb[s] != (int)i ? exp(__ddiv_rn(-(double)(uint32_t)pr.y, sg2)) : 0.0;
-          const double w1 =
-              nb[s + 1] != (int)i ? exp(__ddiv_rn(-(double)(uint32_t)pr.w, sg2)) : 0.0;
+          const double q0 = sg_rcp ? div_rcp(-(double)(uint32_t)pr.y, sg2, rsg2)
+                                   : __ddiv_rn(-(double)(uint32_t)pr.y, sg2);
+          const double q1 = sg_rcp ? div_rcp(-(double)(uint32_t)pr.w, sg2, rsg2)
+                                   : __ddiv_rn(-(double)(uint32_t)pr.w, sg2);
+          const double w0 = nb[s] != (int)i ? exp(q0) : 0.0;
+          const double w1 = nb[s + 1] != (int)i ? exp(q1) : 0.0;
           pr.y = __float_as_int((float)w0);
           pr.w = __float_as_int((float)w1);
           *reinterpret_cast<int4*>(ell.nbr + eslot(s, n, i)) = pr;
@@ -217,9 +224,9 @@ __global__ void __launch_bounds__(kNe2Warps * 32, 6) k_noise2(const uint32_t* __
     }
     if (valid) {
       // numpy std over the patch axis per channel, then the channel mean
-      fslr[i] = ok ? __ddiv_rn(__dadd_rn(__dadd_rn(patch_std(v, 0, D), patch_std(v, 1, D)),
-                                         patch_std(v, 2, D)),
-                               3.0)
+      fslr[i] = ok ? div_rcp(__dadd_rn(__dadd_rn(patch_std(v, 0, D, rD), patch_std(v, 1, D, rD)),
+                                       patch_std(v, 2, D, rD)),
+                             3.0, r3)
                    : -1.0;
     }
 #pragma unroll
