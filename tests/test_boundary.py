@@ -178,3 +178,21 @@ def test_product_package_never_imports_oracle():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert not re.search(r"^\s*(import|from)\s+oracle|fgbd_oracle", text, re.M), f
+
+
+def test_reciprocal_division_identity(tmp_path):
+    """div_rcp (device_util.cuh) replaces IEEE division by one shared
+    reciprocal + an FMA correction; the identity is checked on the host in C
+    over random and edge-range pairs (exit code 0 = bit-identical)."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = Path(__file__).resolve().parents[1] / "tools" / "micro" / "div_check.c"
+    exe = tmp_path / "div_check"
+    subprocess.run([gcc, "-O2", "-ffp-contract=off", "-o", str(exe), str(src), "-lm"], check=True)
+    out = subprocess.run([str(exe), "20000000"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout
+    assert "bad=0" in out.stdout

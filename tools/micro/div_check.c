@@ -2,6 +2,7 @@
 // (device_util.cuh): RN(a/b) == q0 + FMA residual correction, 3e8 pairs.
 //   gcc -O2 -march=native -ffp-contract=off -o div_check div_check.c -lm
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <stdint.h>
 #include <string.h>
@@ -17,9 +18,10 @@ static double div_rcp(double a, double b, double y) {
   double r = fma(-b, q0, a);
   return fma(r, y, q0);
 }
-int main(){
+int main(int argc, char** argv){
   long bad = 0, n = 0;
-  for (long it = 0; it < 300000000L; ++it) {
+  const long iters = argc > 1 ? atol(argv[1]) : 300000000L;
+  for (long it = 0; it < iters; ++it) {
     double a, b;
     switch (it % 6) {
       case 0: b = (double)(2 + xr() % 6); a = u01() * 1785.0; break;              // patch sums / D
@@ -36,4 +38,5 @@ int main(){
     if (x1 != x2 && !(isnan(q) && isnan(ref))) { if (bad < 5) printf("a=%a b=%a q=%a ref=%a\n", a, b, q, ref); ++bad; }
   }
   printf("n=%ld bad=%ld\n", n, bad);
+  return bad != 0;
 }
