@@ -544,27 +544,32 @@ static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coord
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
   if ((rc = ensure_capacity(ctx, n, 3 * bits > 32))) return rc;
   apply_l2_policy(ctx, n);
-  if (!dev && (rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false))) return rc;
-  if (!dev) FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   const int64_t* frame_coords = dev ? coords : ctx->coords64;
   // static-geometry reuse: the held graph stands if this frame's coordinates
   // are byte-identical to the ones it was built from (exact device compare)
   const bool want_reuse = (flags & FGBD_FLAG_REUSE_GRAPH) && !slab && !w64;
-  bool reuse = false;
-  if (want_reuse && ctx->held_valid && ctx->g_n == n && ctx->g_bits == bits &&
-      ctx->g_have_weights && !ctx->g_weights64) {
-    int same = 0;
-    if ((rc = coords_equal(ctx, frame_coords, ctx->held_coords, 3 * n, &same))) return rc;
-    reuse = same != 0;
-  }
-  // without a graph build there is nothing for the colour upload to hide
-  // behind: move it ahead of the device lock (other contexts' kernels run)
+  const bool may_reuse = want_reuse && ctx->held_valid && ctx->g_n == n && ctx->g_bits == bits &&
+                         ctx->g_have_weights && !ctx->g_weights64;
+  // A frame that will probably reuse the graph has no build for the colour
+  // upload to hide behind, so its colours travel ahead of the device lock,
+  // together with the coordinates.  Both copies go before the compare
+  // kernel: copies need only the copy engines, while a kernel may have to
+  // wait for another context's persistent filter to release the SMs.
   const double* frame_colors = colors;
   bool colors_dev = dev;
-  if (reuse && !dev) {
+  if (!dev && (rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false))) return rc;
+  if (may_reuse && !dev) {
     if ((rc = h2d(ctx, ctx->out, colors, 3 * n * sizeof(double), false))) return rc;
     frame_colors = ctx->out;
     colors_dev = true;
+  }
+  bool reuse = false;
+  if (may_reuse) {
+    int same = 0;  // syncs the stream: coordinates (and colours) have landed
+    if ((rc = coords_equal(ctx, frame_coords, ctx->held_coords, 3 * n, &same))) return rc;
+    reuse = same != 0;
+  } else if (!dev) {
+    FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   }
   std::unique_lock<std::mutex> compute_lock(device_mutex(ctx->device));
   // the side stream starts after the coordinates have landed (full PCIe
