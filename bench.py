@@ -233,6 +233,7 @@ def run_b200(args):
     nnz = int(rep0.nnz)
     # dominant kernel: the filter step, event-timed inside the library
     lf_s = float(np.mean([r.t_lf_steps for r in reps])) / max(S, 1)
+    frame_bytes = 144.125 * n + 12.0 * nnz + S * (52.125 * n + 8.0 * nnz)
     lf_bytes = 52.125 * n + 8.0 * nnz
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -328,6 +329,14 @@ def run_b200(args):
                          "algorithmic_bytes_per_launch": lf_bytes,
                          "launch_ms": lf_s * 1e3, "peak_source": "MEASURED_PEAKS.json hbm_gbs"
                          if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"},
+            # whole-frame algorithmic bytes: GC 88N+8nnz, NE 48N+4nnz,
+            # FSLR 8.125N, S x (52.125N + 8nnz)
+            "frame_roofline": {
+                "bytes_per_frame": frame_bytes,
+                "achieved": frame_bytes / (total_ms / args.steps / 1e3) / 1e9, "peak": peak,
+                "unit": "GB/s",
+                "frac": frame_bytes / (total_ms / args.steps / 1e3) / 1e9 / peak,
+                "roofline_fps": peak * 1e9 / frame_bytes},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "parity": parity,
         }
