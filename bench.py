@@ -302,7 +302,11 @@ def run_b200(args):
         t_cpu = time.perf_counter() - t0
         cpu = {"value": 1.0 / t_cpu, "unit": "frames/s", "cores": 1, "kind": "port",
                "sample": f"1 frame of the same workload ({n:,} pts, S={ref.steps}), "
-                         f"{t_cpu:.2f} s single-threaded numpy oracle"}
+                         f"{t_cpu:.2f} s single-threaded numpy/scipy oracle",
+               "stage_s": {k: round(v, 4) for k, v in (ref.stage_timings or {}).items()},
+               "host_cores_visible": len(os.sched_getaffinity(0)),
+               "thread_env": {k: os.environ.get(k) for k in
+                              ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "NUMBA_NUM_THREADS")}}
         out_d = d_out.cpu().numpy()
         parity = {"q_gpu": q, "q_ref": ref.selected_q, "S_gpu": S, "S_ref": ref.steps,
                   "sigma_est_rel": abs(rep0.sigma_est - ref.sigma_est) / ref.sigma_est,
