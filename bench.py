@@ -180,8 +180,8 @@ def run_b200(args):
     ctx = nat.context()
     stream = torch.cuda.ExternalStream(ctx.lib.fgbd_ctx_stream(ctx.handle), device=local)
     dev = torch.device("cuda", local)
-    d_coords = torch.from_numpy(np.ascontiguousarray(noisy.coords)).to(dev)
-    d_colors = torch.from_numpy(np.ascontiguousarray(noisy.colors)).to(dev)
+    d_coords = torch.from_numpy(np.array(noisy.coords)).to(dev)
+    d_colors = torch.from_numpy(np.array(noisy.colors)).to(dev)
     d_out = torch.empty((n, 3), dtype=torch.float64, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     cfg = nat.make_config(fb.FilterConfig())
