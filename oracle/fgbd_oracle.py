@@ -326,6 +326,14 @@ def patch_covariance(x: np.ndarray) -> np.ndarray:
     return (s + s.T) * 0.5
 
 
+# noise.py:152's off-diagonal norm is a difference of two sums and cannot
+# resolve below ~sqrt(ulp(|a|^2)); the reference then reports non-convergence
+# for matrices whose off-diagonal entries are exactly zero.  The CUDA path
+# accepts such a matrix; tests set this flag to compute
+# the result it must match.  Default False: the oracle is the reference.
+JACOBI_DIRECT_OFF_FALLBACK = False
+
+
 def symmetric_eigenvalues(s: np.ndarray, max_sweeps: int = JACOBI_MAX_SWEEPS) -> np.ndarray:
     """Cyclic Jacobi, descending eigenvalues (noise.py:133-185).
 
@@ -375,6 +383,8 @@ def symmetric_eigenvalues(s: np.ndarray, max_sweeps: int = JACOBI_MAX_SWEEPS) ->
                 a[q, :] = sn * rp + c * rq
                 a[p, q] = a[q, p] = 0.0
     if off_norm() <= tol:
+        return np.sort(np.diag(a))[::-1]
+    if JACOBI_DIRECT_OFF_FALLBACK and math.sqrt(float(np.sum((a - np.diag(np.diag(a))) ** 2))) <= tol:
         return np.sort(np.diag(a))[::-1]
     raise OracleError("noise", f"Jacobi did not converge in {max_sweeps} sweeps")
 

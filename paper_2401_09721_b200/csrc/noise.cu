@@ -304,6 +304,25 @@ int launch_noise(fgbd_ctx* ctx, int64_t n, int patch, int fuse_weights) {
 
 static double np_sign(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
 
+// numpy's add.reduce over a contiguous float64 vector of n <= 128 values
+// (pairwise_sum: n < 8 sequential from 0; else 8 strided accumulators,
+// combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail sequentially)
+static double np_pairwise_sum(const double* x, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res += x[i];
+    return res;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = x[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] += x[i + j];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res += x[i];
+  return res;
+}
+
 int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err) {
   // symmetry check on the raw input (noise.py:142-144)
   double scale = 0.0, asym = 0.0;
@@ -329,9 +348,18 @@ int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* er
     return FGBD_OK;
   }
   const double target = 1e-12 * norm;
+  // noise.py:152: sqrt(max(np.sum(a * a) - np.sum(np.diag(a) ** 2), 0)).  The
+  // difference cancels catastrophically near convergence (|a|^2 ~ 1e7 leaves
+  // an absolute error ~1e-9, i.e. off ~ 1e-4 >> the 1e-12 |a| target), so
+  // whether the reference converges or reports a failure is decided by the
+  // rounding of these two sums: reproduce numpy's order exactly -- pairwise
+  // (8 strided accumulators) over the d*d products, sequential over the
+  // diagonal (fewer than 8 terms).
   auto off_norm = [&]() {
-    double all = 0.0, dg = 0.0;
-    for (int i = 0; i < d * d; ++i) all += a[i] * a[i];
+    double sq[49];
+    for (int i = 0; i < d * d; ++i) sq[i] = a[i] * a[i];
+    const double all = np_pairwise_sum(sq, d * d);
+    double dg = 0.0;
     for (int i = 0; i < d; ++i) dg += a[i * d + i] * a[i * d + i];
     return std::sqrt(std::max(all - dg, 0.0));
   };
@@ -378,7 +406,17 @@ int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* er
     }
   }
   const double off = off_norm();
-  if (off <= target) {
+  // The difference-of-sums norm above has a floor of ~sqrt(ulp(|a|^2)): on
+  // some matrices the reference reports non-convergence (noise.py:179-185)
+  // while its off-diagonal entries are all exactly zero, and which matrices
+  // hit this depends on the last ulp of the covariance (i.e. on the BLAS
+  // build).  Only a matrix whose off-diagonal norm, summed directly, is still
+  // above the target is reported as a failure; see DESIGN.md "Parity".
+  double off_direct = 0.0;
+  for (int p = 0; p < d; ++p)
+    for (int q = 0; q < d; ++q)
+      if (p != q) off_direct += a[p * d + q] * a[p * d + q];
+  if (off <= target || std::sqrt(off_direct) <= target) {
     finish();
     return FGBD_OK;
   }
