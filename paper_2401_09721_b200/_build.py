@@ -37,10 +37,15 @@ def _headers():
     return list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False,
+          defines: tuple = (), lib: Path | None = None) -> Path:
+    """Build the library; `defines`/`lib` make an experiment variant (e.g.
+    ("FGBD_LF_TLOG=1",) -> tools/_lib_tlog.so) in its own object directory."""
     nvcc = _nvcc()
     OUT_DIR.mkdir(exist_ok=True)
-    obj_dir = ROOT / "build" / "obj"
+    LIB_OUT = Path(lib) if lib else LIB
+    tag = "_".join(d.replace("=", "") for d in defines)
+    obj_dir = ROOT / "build" / ("obj_" + tag if tag else "obj")
     obj_dir.mkdir(parents=True, exist_ok=True)
     hdr_mtime = max((h.stat().st_mtime for h in _headers()), default=0)
     objs = []
@@ -51,21 +56,22 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
         objs.append(o)
         if not force and o.exists() and o.stat().st_mtime >= max(s.stat().st_mtime, hdr_mtime):
             continue
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(s), "-o", str(o)]
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], f"-I{INCLUDE}", f"-I{CSRC}",
+               "-c", str(s), "-o", str(o)]
         if ptxas_v:
             cmd[1:1] = ["-Xptxas", "-v"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
         rebuilt = True
-    if rebuilt or force or not LIB.exists():
-        tmp = LIB.with_suffix(".so.tmp")
+    if rebuilt or force or not LIB_OUT.exists():
+        tmp = LIB_OUT.with_suffix(".so.tmp")
         cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-cudart", "static"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, LIB_OUT)
+    return LIB_OUT
 
 
 if __name__ == "__main__":

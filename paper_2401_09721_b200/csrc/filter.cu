@@ -37,6 +37,15 @@
 #ifndef FGBD_LF_SIGHINT
 #define FGBD_LF_SIGHINT 1
 #endif
+#ifndef FGBD_LF_PF
+// software prefetch in the filter sweep (experiment): bit 0 = the next row's
+// own and neighbour signal rows into L1 while this row's gathers are in
+// flight; bit 1 = the graph rows two iterations ahead into L2
+#define FGBD_LF_PF 2
+#endif
+#ifndef FGBD_LF_PFD
+#define FGBD_LF_PFD 2  // prefetch distance of bits 1 / 2, in sweep iterations
+#endif
 #include "device_util.cuh"
 #include "fgbd_internal.cuh"
 
@@ -286,8 +295,17 @@ __device__ __forceinline__ void load_row_slots(const StepArgs& a, int64_t i, uin
 }
 
 // out = (d f + sum_s w_s f_s) / (2 d), the reference's order (filtering.py:132-155).
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const float (&wf)[kSlots],
-                                                  const double4* in, int64_t i, uint64_t pol_keep) {
+                                                  const double4* in, int64_t i, uint64_t pol_keep,
+                                                  const int* pf_nb = nullptr,
+                                                  int64_t pf_i = -1) {
   const double4 f = ld_row_hint(in + i, pol_keep);
   double4 g[kSlots];
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
@@ -303,6 +321,11 @@ __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const
 #else
     g[s] = ld_row(in + ell_j(nb[s]));
 #endif
+  if ((FGBD_LF_PF & 1) && pf_i >= 0) {
+    prefetch_l1(in + pf_i);
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) prefetch_l1(in + ell_j(pf_nb[s]));
+  }
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
     // the ELL word's bit 31 says whether the neighbour's ORIGINAL index is
@@ -432,7 +455,31 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
     }
     const int64_t inext = i + stride;
     if (inext < end) load_row_slots<WM>(a, inext, pol_stream, neg_inv_sg2, nbn, wn);
+#if FGBD_LF_PF & 2
+    if (i + FGBD_LF_PFD * stride < end)
+#pragma unroll
+      for (int s = 0; s < kSlots; s += 2)
+        prefetch_l2(a.E.nbr + eslot(s, n, i + FGBD_LF_PFD * stride));
+#endif
+#if FGBD_LF_PF & 4
+    // one bulk L2 prefetch per graph plane for the whole block's rows
+    // FGBD_LF_PFD iterations ahead (thread 0 of each block)
+    if (threadIdx.x == 0 && a.chunk > 0) {
+      const int64_t r0 = i + FGBD_LF_PFD * stride;
+      const int64_t r1 = min(end, r0 + stride);
+      if (r0 < r1)
+#pragma unroll
+        for (int s = 0; s < kSlots; s += 2)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.E.nbr + eslot(s, n, r0)),
+                       "r"((uint32_t)((r1 - r0) * 16))
+                       : "memory");
+    }
+#endif
+#if FGBD_LF_PF & 1
+    const double4 o = row_from_slots(nbc, wc, in, i, pol_keep, nbn, inext < end ? inext : -1);
+#else
     const double4 o = row_from_slots(nbc, wc, in, i, pol_keep);
+#endif
     st_row_hint(out + i, o, pol_keep);
     if (SUMS && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
       sx[0] = fma(o.x, o.x, sx[0]);
@@ -628,6 +675,27 @@ __device__ __forceinline__ void sweep_tma(const StepArgs& a, const double4* in, 
 // criterion decision for step c waits for every block's step-c flag, one
 // step later, and reads partials from a 4-deep ring (no block is more than
 // two steps ahead of any other).
+#if FGBD_LF_TLOG
+// Timeline instrumentation (experiment builds only, -DFGBD_LF_TLOG=1): per
+// step c < kTlogSteps and block, %globaltimer at step start, sweep end and
+// barrier entry.  Read back with fgbd_debug_tlog (tools/lf_timeline.py).
+constexpr int kTlogSteps = 16;
+__device__ unsigned long long g_tlog[kTlogSteps][kMaxCoopBlocks][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TLOG(c, k)                                                            \
+  do {                                                                        \
+    if (threadIdx.x == 0 && (c) < kTlogSteps) g_tlog[(c)][blockIdx.x][(k)] = gtimer(); \
+  } while (0)
+#else
+#define TLOG(c, k) \
+  do {             \
+  } while (0)
+#endif
+
 template <int WM, bool SELECT, int BLK = kBlock, int MINB = 3, bool TMA = false,
           bool P2P = false>
 __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
@@ -700,6 +768,14 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   }
   int c = s_st.q;  // x_c complete and decided (c = 0 at entry)
   bool decided = true;
+  // thread 0: the criterion of x_c from its totals, and the selection update
+  auto decide = [&](const double (&t)[3]) {
+    const double crit = criterion(s_sy, t, s_inc, s_sv2, s_mode);
+    s_st.out_b = s_st.in_b;  // x_c's buffer becomes the best if crit_c improves
+    s_st.q = c - 1;
+    select_update(s_st, crit, s_qmax, s_early);
+    if (blockIdx.x == 0 && c < FGBD_TRACE_MAX) ctl->trace[c] = crit;
+  };
   while (!s_st.stop) {
     if (kBulkPart && !decided && threadIdx.x == 0) {
       const uint32_t bytes = (uint32_t)(pstride * 8);
@@ -711,6 +787,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     int ob = BUF_A;
     if (ob == ib || ob == bb) ob = BUF_B;
     if (ob == ib || ob == bb) ob = BUF_Y;
+    TLOG(c, 0);
     if (c < s_qmax) {
       double sx[3] = {0.0, 0.0, 0.0};
       if (TMA)
@@ -719,6 +796,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
         sweep<WM, SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx);
       if (SELECT) {
         block_sum<3>(sx, s_red);
+        TLOG(c, 1);
         if (threadIdx.x == 0)
           for (int k = 0; k < 3; ++k)
             a.part[((c + 1) & (kRing - 1)) * (kBulkPart ? pstride : 3 * nb) + k * nb + blockIdx.x] =
@@ -748,13 +826,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
           for (int k = 0; k < 3; ++k) t[k] += __ldcg(&part[k * nb + b]);
       }
       block_sum<3>(t, s_red);
-      if (threadIdx.x == 0) {
-        const double crit = criterion(s_sy, t, s_inc, s_sv2, s_mode);
-        s_st.out_b = s_st.in_b;  // x_c's buffer becomes the best if crit_c improves
-        s_st.q = c - 1;
-        select_update(s_st, crit, s_qmax, s_early);
-        if (blockIdx.x == 0 && c < FGBD_TRACE_MAX) ctl->trace[c] = crit;
-      }
+      if (threadIdx.x == 0) decide(t);
       __syncthreads();
     }
     if (!SELECT && c >= s_qmax) break;
@@ -764,6 +836,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       // published; the acquire orders this block's next loads after it
       wait_blocks(a.flags, s_dep_lo, s_dep_hi, blockIdx.x, a.base + c + 1);
     } else {
+      TLOG(c, 2);
       grid.sync();
     }
     if (threadIdx.x == 0) {
@@ -1118,3 +1191,9 @@ int launch_criterion(fgbd_ctx* ctx, const double* d_y, const double* d_x, const 
 }
 
 }  // namespace fgbd
+
+#if FGBD_LF_TLOG
+extern "C" int fgbd_debug_tlog(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, fgbd::g_tlog, sizeof(fgbd::g_tlog));
+}
+#endif
