@@ -147,6 +147,28 @@ struct SortPass {
 constexpr unsigned long long kFlagAgg = 1ull << 32;
 constexpr unsigned long long kFlagPre = 2ull << 32;
 
+#if FGBD_SORT_TLOG
+// Timeline instrumentation (experiment builds only, -DFGBD_SORT_TLOG=1):
+// %globaltimer per (pass, line, tile) at block start, after the multisplit,
+// after the look-back and at the end.  Read back with fgbd_debug_stlog.
+constexpr int kStlogTiles = 1024;
+__device__ unsigned long long g_stlog[4][3][kStlogTiles][4];
+__device__ __forceinline__ unsigned long long sort_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define STLOG(k)                                                                  \
+  do {                                                                            \
+    if (threadIdx.x == 0 && p.pass < 4 && s_tile < kStlogTiles)                   \
+      g_stlog[p.pass][blockIdx.y][s_tile][(k)] = sort_timer();                    \
+  } while (0)
+#else
+#define STLOG(k) \
+  do {           \
+  } while (0)
+#endif
+
 template <typename K, bool FIRST, bool LAST, bool SLG>
 __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortPass p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -163,6 +185,7 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   if (tid == 0) s_tile = (int)atomicAdd(&p.tile_ctr[line], 1u);
   for (int t = tid; t < 8 * kRadix; t += kSortThreads) s_whist[t] = 0;
   __syncthreads();
+  STLOG(0);
   const int tile = s_tile;
   const int64_t base = (int64_t)tile * kSortTile;
   const int shift = 8 * p.pass;
@@ -216,6 +239,7 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
     s_whist[w * kRadix + d] = count;
     count += c;
   }
+  STLOG(1);
   // decoupled look-back over preceding tiles of this line
   unsigned long long* st = p.status + ((int64_t)line * p.tiles) * kRadix;
   const unsigned long long ep = (unsigned long long)p.epoch << 34;
@@ -265,6 +289,7 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   s_start[d] = start;
   s_gofs[d] = p.bases[(line * p.passes + p.pass) * kRadix + d] + excl - start;
   __syncthreads();
+  STLOG(2);  // every digit's look-back is done
   // reorder the tile in shared memory by digit (stable)
 #pragma unroll
   for (int j = 0; j < kSortIPT; ++j) {
@@ -289,6 +314,10 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
     if (!LAST) kout[g] = kk;
     vout[g] = s_vals[i];
   }
+#if FGBD_SORT_TLOG
+  __syncthreads();
+  STLOG(3);
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -885,3 +914,9 @@ int launch_export(fgbd_ctx* ctx, int64_t n, int64_t* d_indptr, int64_t* d_indice
 }
 
 }  // namespace fgbd
+
+#if FGBD_SORT_TLOG
+extern "C" int fgbd_debug_stlog(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, fgbd::g_stlog, sizeof(fgbd::g_stlog));
+}
+#endif
