@@ -38,13 +38,17 @@
 #define FGBD_LF_SIGHINT 1
 #endif
 #ifndef FGBD_LF_PF
-// software prefetch in the filter sweep (experiment): bit 0 = the next row's
-// own and neighbour signal rows into L1 while this row's gathers are in
-// flight; bit 1 = the graph rows two iterations ahead into L2
-#define FGBD_LF_PF 2
+// prefetch.global.L2 of the graph row FGBD_LF_PFD sweep iterations ahead
+// (profiles/r1_summary.md, r1c: -2.4% filter time at distance 2)
+#define FGBD_LF_PF 1
 #endif
 #ifndef FGBD_LF_PFD
-#define FGBD_LF_PFD 2  // prefetch distance of bits 1 / 2, in sweep iterations
+#define FGBD_LF_PFD 2
+#endif
+#ifndef FGBD_LF_ELLSMEM
+// graph slots of the next FGBD_LF_ELLSMEM rows via cp.async into shared memory (0: registers;
+// profiles/r1_summary.md r1c: 1 stage -2.5% filter time, 2 / 3 stages slower -- less L1)
+#define FGBD_LF_ELLSMEM 1
 #endif
 #include "device_util.cuh"
 #include "fgbd_internal.cuh"
@@ -295,17 +299,12 @@ __device__ __forceinline__ void load_row_slots(const StepArgs& a, int64_t i, uin
 }
 
 // out = (d f + sum_s w_s f_s) / (2 d), the reference's order (filtering.py:132-155).
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const float (&wf)[kSlots],
-                                                  const double4* in, int64_t i, uint64_t pol_keep,
-                                                  const int* pf_nb = nullptr,
-                                                  int64_t pf_i = -1) {
+                                                  const double4* in, int64_t i, uint64_t pol_keep) {
   const double4 f = ld_row_hint(in + i, pol_keep);
   double4 g[kSlots];
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
@@ -321,11 +320,7 @@ __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const
 #else
     g[s] = ld_row(in + ell_j(nb[s]));
 #endif
-  if ((FGBD_LF_PF & 1) && pf_i >= 0) {
-    prefetch_l1(in + pf_i);
-#pragma unroll
-    for (int s = 0; s < kSlots; ++s) prefetch_l1(in + ell_j(pf_nb[s]));
-  }
+
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) {
     // the ELL word's bit 31 says whether the neighbour's ORIGINAL index is
@@ -423,12 +418,20 @@ __device__ __forceinline__ double4* pick_buf(const StepArgs& a, int b) {
   return b == 0 ? a.buf[0] : (b == 1 ? a.buf[1] : a.buf[2]);
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
 // One sweep of this block's rows: out = P in, optionally summing out^2 over
 // included rows.  The next row's graph slots are fetched while the current
-// row's neighbour gathers are in flight.
+// row's neighbour gathers are in flight (into registers, or with
+// FGBD_LF_ELLSMEM by cp.async into this thread's shared-memory slots, which
+// frees 12 registers), and the graph row FGBD_LF_PFD iterations ahead is
+// prefetched into L2.
 template <int WM, bool SUMS>
 __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, double4* out,
-                                      bool mask_all, float neg_inv_sg2, double (&sx)[3]) {
+                                      bool mask_all, float neg_inv_sg2, double (&sx)[3],
+                                      int4* s_ell) {
   const int64_t n = a.n;
   // rows of this block: a contiguous range walked in blockDim strides (the
   // neighbours of raster / scan-ordered clouds then mostly hit this SM's L1),
@@ -444,42 +447,58 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
     stride = (int64_t)gridDim.x * blockDim.x;
   }
   const uint64_t pol_stream = graph_policy(), pol_keep = policy_evict_last();
+  constexpr bool kSmemEll = FGBD_LF_ELLSMEM && WM == W_STORED;
   int nbc[kSlots], nbn[kSlots];
   float wc[kSlots], wn[kSlots];
-  if (i < end) load_row_slots<WM>(a, i, pol_stream, neg_inv_sg2, nbn, wn);
-  while (i < end) {
+  // shared-memory slots [stage][pair][thread]: each thread reads back only
+  // what it copied itself, so no block barrier is needed
+  constexpr int NS = FGBD_LF_ELLSMEM + 1;  // stages: rows in flight + the one in use
+  const int T = blockDim.x;
+  int stage = 0;
+  auto issue = [&](int64_t r, int st) {
+    if (r < end)
 #pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
-      nbc[s] = nbn[s];
-      wc[s] = wn[s];
-    }
+      for (int s = 0; s < kSlots; s += 2)
+        asm volatile(
+            "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
+                smem_u32(s_ell + (st * 3 + (s >> 1)) * T + threadIdx.x)),
+            "l"(a.E.nbr + eslot(s, n, r)), "l"(pol_stream)
+            : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if constexpr (kSmemEll) {
+#pragma unroll
+    for (int k = 0; k < NS - 1; ++k) issue(i + k * stride, k);
+  } else if (i < end) {
+    load_row_slots<WM>(a, i, pol_stream, neg_inv_sg2, nbn, wn);
+  }
+  while (i < end) {
     const int64_t inext = i + stride;
-    if (inext < end) load_row_slots<WM>(a, inext, pol_stream, neg_inv_sg2, nbn, wn);
-#if FGBD_LF_PF & 2
-    if (i + FGBD_LF_PFD * stride < end)
+    if constexpr (kSmemEll) {
+      issue(i + (NS - 1) * stride, stage == 0 ? NS - 1 : stage - 1);
+      asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1) : "memory");
+#pragma unroll
+      for (int s = 0; s < kSlots; s += 2) {
+        const int4 pr = s_ell[(stage * 3 + (s >> 1)) * T + threadIdx.x];
+        nbc[s] = pr.x;
+        wc[s] = __int_as_float(pr.y);
+        nbc[s + 1] = pr.z;
+        wc[s + 1] = __int_as_float(pr.w);
+      }
+      stage = stage + 1 == NS ? 0 : stage + 1;
+    } else {
+#pragma unroll
+      for (int s = 0; s < kSlots; ++s) {
+        nbc[s] = nbn[s];
+        wc[s] = wn[s];
+      }
+      if (inext < end) load_row_slots<WM>(a, inext, pol_stream, neg_inv_sg2, nbn, wn);
+    }
+    if (FGBD_LF_PF && i + FGBD_LF_PFD * stride < end)
 #pragma unroll
       for (int s = 0; s < kSlots; s += 2)
         prefetch_l2(a.E.nbr + eslot(s, n, i + FGBD_LF_PFD * stride));
-#endif
-#if FGBD_LF_PF & 4
-    // one bulk L2 prefetch per graph plane for the whole block's rows
-    // FGBD_LF_PFD iterations ahead (thread 0 of each block)
-    if (threadIdx.x == 0 && a.chunk > 0) {
-      const int64_t r0 = i + FGBD_LF_PFD * stride;
-      const int64_t r1 = min(end, r0 + stride);
-      if (r0 < r1)
-#pragma unroll
-        for (int s = 0; s < kSlots; s += 2)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.E.nbr + eslot(s, n, r0)),
-                       "r"((uint32_t)((r1 - r0) * 16))
-                       : "memory");
-    }
-#endif
-#if FGBD_LF_PF & 1
-    const double4 o = row_from_slots(nbc, wc, in, i, pol_keep, nbn, inext < end ? inext : -1);
-#else
     const double4 o = row_from_slots(nbc, wc, in, i, pol_keep);
-#endif
     st_row_hint(out + i, o, pol_keep);
     if (SUMS && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
       sx[0] = fma(o.x, o.x, sx[0]);
@@ -488,6 +507,7 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
     }
     i = inext;
   }
+  if constexpr (kSmemEll) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -507,9 +527,6 @@ constexpr int kWinRows = kTile + 2 * kHaloMax;
 constexpr int kStageBytes = kWinRows * 32 + 3 * kTile * 16;
 constexpr int kTmaSmem = 128 + 2 * kStageBytes;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
                : "memory");
@@ -707,6 +724,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     mbar_init(&tma.bar[1], 1);
   }
   __shared__ double s_red[32 * 3];
+  // graph-slot stages of the sweep (dynamic shared memory, FGBD_LF_ELLSMEM)
+  int4* s_ell = reinterpret_cast<int4*>(dyn_smem);
   __shared__ SelState s_st;
   __shared__ double s_sy[3], s_sv2;
   __shared__ long long s_inc;
@@ -793,7 +812,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       if (TMA)
         sweep_tma<SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, tma, sx);
       else
-        sweep<WM, SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx);
+        sweep<WM, SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx, s_ell);
       if (SELECT) {
         block_sum<3>(sx, s_red);
         TLOG(c, 1);
@@ -1053,13 +1072,15 @@ static StepArgs step_args(fgbd_ctx* ctx, int64_t n) {
 template <int WM, bool SELECT, int BLK, int MINB, bool TMA = false, bool P2P = false>
 static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
   auto kern = k_lf_run<WM, SELECT, BLK, MINB, TMA, P2P>;
-  const int smem = TMA ? kTmaSmem : 0;
+  constexpr int kEllSmem = (FGBD_LF_ELLSMEM && WM == W_STORED) ? (FGBD_LF_ELLSMEM + 1) * 3 * BLK * 16 : 0;
+  const int smem = TMA ? kTmaSmem : kEllSmem;
   if (ctx->coop_blocks[slot] == 0) {
-    if (TMA) {
+    if (TMA || kEllSmem > 0) {
       FGBD_CUDA(ctx, cudaFuncSetAttribute((const void*)kern,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      FGBD_CUDA(ctx, cudaFuncSetAttribute((const void*)kern,
-                                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      if (TMA)
+        FGBD_CUDA(ctx, cudaFuncSetAttribute((const void*)kern,
+                                            cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
     int per_sm = 0;
     FGBD_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLK, smem));
@@ -1086,14 +1107,14 @@ static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
 }
 
 // block shape of the persistent kernel (FGBD_LF_SHAPE): 0 = 256 x 3/SM,
-// 1 = 256 x 4/SM (64 registers), 2 = 384 x 2/SM, 3 = 512 x 2/SM (64 registers)
+// 1 = 256 x 4/SM (64 registers), 2 = 288 x 3/SM (75 registers), 3 = 256 x 2/SM (128 registers)
 template <int WM, bool SELECT>
 static int launch_run(fgbd_ctx* ctx, StepArgs& a) {
   const int base = (WM * 2 + (SELECT ? 1 : 0)) * 4 + ctx->lf_shape;
   switch (ctx->lf_shape) {
     case 1: return launch_run_k<WM, SELECT, 256, 4>(ctx, a, base);
-    case 2: return launch_run_k<WM, SELECT, 384, 2>(ctx, a, base);
-    case 3: return launch_run_k<WM, SELECT, 512, 2>(ctx, a, base);
+    case 2: return launch_run_k<WM, SELECT, 288, 3>(ctx, a, base);
+    case 3: return launch_run_k<WM, SELECT, 256, 2>(ctx, a, base);
     default: return launch_run_k<WM, SELECT, 256, 3>(ctx, a, base);
   }
 }
