@@ -26,8 +26,10 @@ def main():
     ap.add_argument("--frames", type=int, default=3)
     ap.add_argument("--cached", type=int, default=-1)
     ap.add_argument("--no-early-exit", action="store_true")
-    ap.add_argument("--order", default="asis", choices=["asis", "shuffle", "morton", "line1"],
-                    help="permute the points before upload (locality experiments)")
+    ap.add_argument("--order", default="asis",
+                    help="permute the points before upload (locality experiments): asis, shuffle, "
+                         "morton, line1, brickN (N^3 voxel bricks in row-major brick order, "
+                         "line-1 order inside a brick), slabN (z slabs of N, line-1 inside)")
     a = ap.parse_args()
     import torch
 
@@ -42,6 +44,14 @@ def main():
             perm = np.random.default_rng(7).permutation(a.n)
         elif a.order == "line1":
             perm = np.lexsort((g[:, 0], g[:, 1], g[:, 2]))
+        elif a.order.startswith("brick"):
+            e = int(a.order[5:])
+            hi = g // e
+            lo = g % e
+            perm = np.lexsort((lo[:, 0], lo[:, 1], lo[:, 2], hi[:, 0], hi[:, 1], hi[:, 2]))
+        elif a.order.startswith("slab"):
+            e = int(a.order[4:])
+            perm = np.lexsort((g[:, 0], g[:, 1], g[:, 2] % e, g[:, 2] // e))
         else:  # morton (z-order) of the voxel coordinates
             def spread(v):
                 v = v.astype(np.uint64) & np.uint64(0x1FFFFF)
