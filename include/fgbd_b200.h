@@ -313,6 +313,16 @@ int32_t fgbd_quantize(fgbd_ctx* ctx, const int64_t* coords_int, const double* co
 int32_t fgbd_sq_error_sum(fgbd_ctx* ctx, const double* a, const double* b, int64_t count,
                           double* sum_out, uint32_t flags);
 
+/* add_gaussian_noise (cloud.py:111-123): out[k] = clip(colors[k] + (0 + sigma z_k),
+ * 0, 255) for the first `count` standard normals z_k of numpy's
+ * Generator(Philox(key, counter)).normal stream (Philox4x64-10 + numpy's
+ * 256-level ziggurat, the same variates bit for bit).  key / counter are the
+ * BitGenerator's state (np.random.Philox(seed).state) before any draw.
+ * sigma < 0 -> FGBD_E_CLOUD. */
+int32_t fgbd_gaussian_noise(fgbd_ctx* ctx, const double* colors, int64_t count, double sigma,
+                            const uint64_t key[2], const uint64_t counter[4], double* out,
+                            uint32_t flags);
+
 /* pinned host buffers for zero-staging transfers */
 void* fgbd_host_alloc(int64_t bytes);
 void fgbd_host_free(void* p);

@@ -221,6 +221,85 @@ def psnr(ref_colors: np.ndarray, test_colors: np.ndarray, cap_db: float = 100.0)
     return float(10.0 * np.log10(255.0 ** 2 / mse))
 
 
+# --------------------------------------------------------------------------
+# add_gaussian_noise (cloud.py:111-123): numpy's Generator(Philox(seed)).normal
+# restated -- Philox4x64-10 (numpy/random/src/philox/philox.h) and the
+# 256-level ziggurat of random_standard_normal (distributions.c).  The third-
+# party algorithm here is numpy's (2.3.5 in this image); the tables are read
+# from numpy's own libnpyrandom.a (tools/gen_ziggurat_tables.py).  Pure Python:
+# small cases only.
+# --------------------------------------------------------------------------
+_M64 = (1 << 64) - 1
+
+
+def philox4x64_10(ctr, key):
+    c, k = list(ctr), list(key)
+    for r in range(10):
+        if r:
+            k = [(k[0] + 0x9E3779B97F4A7C15) & _M64, (k[1] + 0xBB67AE8584CAA73B) & _M64]
+        p0, p1 = 0xD2E7470EE14C6C93 * c[0], 0xCA5A826395121157 * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k[0], p1 & _M64, (p0 >> 64) ^ c[3] ^ k[1], p0 & _M64]
+    return c
+
+
+class PhiloxStream:
+    """numpy's Philox draws from a BitGenerator state (counter, key)."""
+
+    def __init__(self, counter, key):
+        self.ctr = [int(v) for v in counter]
+        self.key = [int(v) for v in key]
+        self.buf: list = []
+
+    def next_u64(self) -> int:
+        if not self.buf:
+            self.ctr[0] = (self.ctr[0] + 1) & _M64
+            i = 0
+            while self.ctr[i] == 0 and i < 3:
+                i += 1
+                self.ctr[i] = (self.ctr[i] + 1) & _M64
+            self.buf = philox4x64_10(self.ctr, self.key)
+        return self.buf.pop(0)
+
+    def next_double(self) -> float:
+        return (self.next_u64() >> 11) * (1.0 / 9007199254740992.0)
+
+
+ZIG_R = 3.6541528853610087963519472518
+ZIG_INV_R = 0.27366123732975827203338247596
+
+
+def standard_normal(st: PhiloxStream, ki, wi, fi) -> float:
+    while True:
+        r = st.next_u64()
+        idx = r & 0xFF
+        r >>= 8
+        rabs = (r >> 1) & 0x000FFFFFFFFFFFFF
+        x = rabs * wi[idx]
+        if r & 1:
+            x = -x
+        if rabs < ki[idx]:
+            return x
+        if idx == 0:
+            while True:
+                xx = -ZIG_INV_R * math.log1p(-st.next_double())
+                yy = -math.log1p(-st.next_double())
+                if yy + yy > xx * xx:
+                    return -(ZIG_R + xx) if (rabs >> 8) & 1 else ZIG_R + xx
+        elif (fi[idx - 1] - fi[idx]) * st.next_double() + fi[idx] < math.exp(-0.5 * x * x):
+            return x
+
+
+def gaussian_noise(colors: np.ndarray, sigma: float, seed: int, ki, wi, fi) -> np.ndarray:
+    """clip(colors + (0 + sigma z), 0, 255) in C order, z from seed's stream."""
+    st0 = np.random.Philox(int(seed)).state["state"]
+    st = PhiloxStream(st0["counter"], st0["key"])
+    flat = np.asarray(colors, np.float64).reshape(-1)
+    out = np.empty_like(flat)
+    for k in range(flat.size):
+        out[k] = min(max(flat[k] + (0.0 + sigma * standard_normal(st, ki, wi, fi)), 0.0), 255.0)
+    return out.reshape(np.shape(colors))
+
+
 def knn_rows(coords: np.ndarray, k: int, queries=None, chunk: int = 256) -> np.ndarray:
     """Exact k nearest neighbours (graph.py:254-285) for the given query rows.
 

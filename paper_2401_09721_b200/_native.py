@@ -121,6 +121,8 @@ _SIGNATURES = {
     "fgbd_quantize": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_i32, C.c_void_p,
                               P(c_i32), c_u32]),
     "fgbd_sq_error_sum": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p, c_i64, P(c_f64), c_u32]),
+    "fgbd_gaussian_noise": (c_i32, [C.c_void_p, C.c_void_p, c_i64, c_f64, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, c_u32]),
     "fgbd_host_alloc": (C.c_void_p, [c_i64]),
     "fgbd_host_free": (None, [C.c_void_p]),
 }
