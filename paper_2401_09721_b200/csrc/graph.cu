@@ -353,19 +353,21 @@ __device__ __forceinline__ void cswap(unsigned& a, unsigned& b) {
   b = hi;
 }
 
-// odd-even transposition sort of 6 values (6 rounds suffice for 6 inputs)
+// sort 6 values: a 12-comparator network of depth 5 (checked on all 2^6
+// 0/1 inputs)
 __device__ __forceinline__ void sort6(unsigned (&c)[6]) {
-#pragma unroll
-  for (int r = 0; r < 6; ++r) {
-    if (r & 1) {
-      cswap(c[1], c[2]);
-      cswap(c[3], c[4]);
-    } else {
-      cswap(c[0], c[1]);
-      cswap(c[2], c[3]);
-      cswap(c[4], c[5]);
-    }
-  }
+  cswap(c[0], c[5]);
+  cswap(c[1], c[3]);
+  cswap(c[2], c[4]);
+  cswap(c[1], c[2]);
+  cswap(c[3], c[4]);
+  cswap(c[0], c[3]);
+  cswap(c[2], c[5]);
+  cswap(c[0], c[1]);
+  cswap(c[2], c[3]);
+  cswap(c[4], c[5]);
+  cswap(c[1], c[2]);
+  cswap(c[3], c[4]);
 }
 
 template <typename K, bool BIG>
@@ -424,13 +426,27 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
     // patch order: rank by (sqdist, index); rows are index-ascending so
     // the slot number breaks ties exactly like the reference's stable sort
     uint32_t order = 0;
+    if (sizeof(K) == 4) {
+      // 3b <= 32: sq < 3 * 2^20, so (sq, slot) packs into one 32-bit key
+      uint32_t key[6];
 #pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      int r = 0;
+      for (int s = 0; s < 6; ++s) key[s] = s < deg ? ((uint32_t)sq[s] << 3) | (uint32_t)s : ~0u;
 #pragma unroll
-      for (int t = 0; t < 6; ++t)
-        r += (t < deg) && (sq[t] < sq[s] || (sq[t] == sq[s] && t < s));
-      if (s < deg) order |= (uint32_t)s << (3 * r);
+      for (int s = 0; s < 6; ++s) {
+        int r = 0;
+#pragma unroll
+        for (int t = 0; t < 6; ++t) r += key[t] < key[s];
+        if (s < deg) order |= (uint32_t)s << (3 * r);
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        int r = 0;
+#pragma unroll
+        for (int t = 0; t < 6; ++t)
+          r += (t < deg) && (sq[t] < sq[s] || (sq[t] == sq[s] && t < s));
+        if (s < deg) order |= (uint32_t)s << (3 * r);
+      }
     }
     // the row of point i (its line-1 rank when rows are reordered) and its
     // neighbours' rows
