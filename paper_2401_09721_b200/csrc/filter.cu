@@ -698,6 +698,7 @@ __device__ __forceinline__ void sweep_tma(const StepArgs& a, const double4* in, 
 // barrier entry.  Read back with fgbd_debug_tlog (tools/lf_timeline.py).
 constexpr int kTlogSteps = 16;
 __device__ unsigned long long g_tlog[kTlogSteps][kMaxCoopBlocks][3];
+__device__ unsigned long long g_wlog[kTlogSteps][kMaxCoopBlocks][16];  // per-warp sweep end
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -813,6 +814,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
         sweep_tma<SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, tma, sx);
       else
         sweep<WM, SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx, s_ell);
+#if FGBD_LF_TLOG
+      if ((threadIdx.x & 31) == 0 && c < kTlogSteps && (threadIdx.x >> 5) < 16)
+        g_wlog[c][blockIdx.x][threadIdx.x >> 5] = gtimer();
+#endif
       if (SELECT) {
         block_sum<3>(sx, s_red);
         TLOG(c, 1);
@@ -1216,5 +1221,8 @@ int launch_criterion(fgbd_ctx* ctx, const double* d_y, const double* d_x, const 
 #if FGBD_LF_TLOG
 extern "C" int fgbd_debug_tlog(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, fgbd::g_tlog, sizeof(fgbd::g_tlog));
+}
+extern "C" int fgbd_debug_wlog(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, fgbd::g_wlog, sizeof(fgbd::g_wlog));
 }
 #endif

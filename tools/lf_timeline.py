@@ -87,6 +87,23 @@ def main():
     print("slowest blocks:", [(int(b), round(float(dur[b]), 2)) for b in order[-6:]])
     q = np.percentile(dur, [0, 25, 50, 75, 100])
     print("mean sweep per block quartiles (us):", np.round(q, 2).tolist())
+    # intra-block spread: per-warp sweep end (lane 0 after its last row)
+    wb = np.zeros((STEPS, MAXB, 16), np.uint64)
+    fw = ctx.lib.fgbd_debug_wlog
+    fw.restype = C.c_int
+    fw.argtypes = [C.c_void_p]
+    assert fw(wb.ctypes.data) == 0
+    w = wb[2:STEPS - 1, :nb, :].astype(np.int64)
+    nw = int(np.count_nonzero(w[0, 0]))
+    w = w[:, :, :nw]
+    st = buf[2:STEPS - 1, :nb, 0].astype(np.int64)[:, :, None]
+    wdur = (w - st) / 1e3
+    spread = wdur.max(axis=2) - wdur.min(axis=2)
+    print(f"warps/block={nw}; per-warp sweep (us) p10/p50/p90 = "
+          f"{np.percentile(wdur, 10):.2f} / {np.median(wdur):.2f} / {np.percentile(wdur, 90):.2f}; "
+          f"intra-block spread (max - min warp) p50 {np.median(spread):.2f}, p90 "
+          f"{np.percentile(spread, 90):.2f}; block mean-warp vs max-warp gap "
+          f"{np.median(wdur.max(axis=2) - wdur.mean(axis=2)):.2f}")
     if a.json:
         Path(a.json).write_text(json.dumps({"rows": rows, "block_sweep_us": dur.round(3).tolist()},
                                            default=float))
