@@ -4,7 +4,7 @@
 //                of all three scan lines for every radix pass (one read)
 //   k_scan_hist  histograms -> exclusive digit bases
 //   k_onesweep   one stable LSD pass for all three lines: warp multisplit
-//                (match.any) -> decoupled look-back across tiles -> smem
+//                (per-bit ballots) -> decoupled look-back across tiles -> smem
 //                reorder -> coalesced scatter (8-bit digits, ceil(3b/8)
 //                passes, exactly the reference's pass count, graph.py:168)
 //   k_neighbors  rank neighbours: cand[l][perm_l[k]] = (perm_l[k-1], perm_l[k+1])
@@ -22,6 +22,9 @@
 
 #ifndef FGBD_LOOK_BATCH
 #define FGBD_LOOK_BATCH 4
+#endif
+#ifndef FGBD_SORT_BALLOT
+#define FGBD_SORT_BALLOT 1  // warp multisplit by per-bit ballots (1) or match.any (0)
 #endif
 #ifndef FGBD_SORT_MINB
 #define FGBD_SORT_MINB 3
@@ -213,12 +216,26 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   }
   // warp multisplit: stable rank of each key among equal digits of its warp
   uint32_t* wh = s_whist + warp * kRadix;
+  const int kwidth = SLG ? 3 * p.b : (int)(sizeof(K) * 8);  // bits above are 0 in every key
+  const int dbits = min(8, max(0, kwidth - shift));
 #pragma unroll
   for (int j = 0; j < kSortIPT; ++j) {
     const int64_t idx = base + (int64_t)warp * 32 * kSortIPT + j * 32 + lane;
     const bool valid = idx < p.n;
     const unsigned d = valid ? (unsigned)((key[j] >> shift) & 0xff) : 0x100u;
+#if FGBD_SORT_BALLOT
+    // lanes with the same 9-bit (valid, digit) value: one ballot per bit
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int bt = 0; bt < 9; ++bt) {
+      if (bt < 8 && bt >= dbits) continue;  // digit bits above the key width are 0
+      const bool on = (d >> bt) & 1u;
+      const unsigned m = __ballot_sync(kFull, on);
+      peers &= on ? m : ~m;
+    }
+#else
     const unsigned peers = __match_any_sync(kFull, d);
+#endif
     const int leader = 31 - __clz(peers);
     uint32_t cnt = 0;
     if (valid && lane == leader) {
