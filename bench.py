@@ -60,7 +60,8 @@ def parse():
                     help="frame: BASELINE configs[1] (default); video: configs[3]; "
                          "slab: configs[4] (one frame split over the GPUs)")
     ap.add_argument("--frames", type=int, default=300, help="video length (configs[3])")
-    ap.add_argument("--workers", type=int, default=2, help="host threads per GPU (video)")
+    ap.add_argument("--workers", type=int, default=None,
+                    help="host threads per GPU (default: video 3, ply 2)")
     ap.add_argument("--no-reuse", action="store_true",
                     help="video/ply: rebuild the graph of every frame even when the geometry is static")
     return ap.parse_args()
@@ -412,6 +413,8 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 
 def run_video(args):
+    if args.workers is None:
+        args.workers = 3  # GPU-ordered frames: 3 host threads keep transfers and compute overlapped
     import torch
 
     import paper_2401_09721_b200 as fb
@@ -496,6 +499,8 @@ def run_video(args):
 # ---------------------------------------------------------------------------
 
 def run_ply(args):
+    if args.workers is None:
+        args.workers = 2  # host-side PLY framing: a third thread costs more than it overlaps
     import torch
 
     import paper_2401_09721_b200 as fb

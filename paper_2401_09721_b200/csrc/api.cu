@@ -341,6 +341,14 @@ std::mutex& device_mutex(int device) {
   return m[device & 63];
 }
 
+// The last frame compute enqueued on each device (guarded by device_mutex):
+// the next frame's stream waits for it on the GPU, so a frame whose compute
+// needs no host round trip can release the lock as soon as it is enqueued.
+cudaEvent_t& device_last_compute(int device) {
+  static cudaEvent_t ev[64] = {};
+  return ev[device & 63];
+}
+
 double ev_sec(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
@@ -419,6 +427,8 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
     return fail(e, "side stream");
   if ((e = cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming)) != cudaSuccess)
     return fail(e, "side event");
+  if ((e = cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming)) != cudaSuccess)
+    return fail(e, "event");
   if ((e = cudaEventCreateWithFlags(&ctx->ev_perm, cudaEventDisableTiming)) != cudaSuccess)
     return fail(e, "perm event");
   for (auto& ev : ctx->ev)
@@ -438,6 +448,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_NE_VARIANT")) ctx->ne_variant = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_SHAPE")) ctx->lf_shape = std::atoi(v) & 3;
   if (const char* v = std::getenv("FGBD_LF_CHUNK")) ctx->lf_chunk = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_ASYNC_LOCK")) ctx->async_lock = std::atoi(v);
   if (const char* v = std::getenv("FGBD_REORDER")) ctx->reorder_rows = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_HALO")) ctx->lf_halo = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
@@ -471,6 +482,14 @@ void fgbd_ctx_destroy(fgbd_ctx* ctx) {
   if (ctx->side) cudaStreamSynchronize(ctx->side);
   if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
   if (ctx->ev_perm) cudaEventDestroy(ctx->ev_perm);
+  if (ctx->ev_done) {
+    std::lock_guard<std::mutex> lk(device_mutex(ctx->device));
+    if (device_last_compute(ctx->device) == ctx->ev_done) {
+      cudaEventSynchronize(ctx->ev_done);
+      device_last_compute(ctx->device) = nullptr;
+    }
+    cudaEventDestroy(ctx->ev_done);
+  }
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -577,6 +596,10 @@ static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coord
   // staging buffers; it then overlaps the colour upload with the graph build
   FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->stream));
   FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_side, 0));
+  // this frame's compute starts after the previous frame's on the device
+  // (the colour upload on the side stream need not wait for it)
+  if (cudaEvent_t prev = device_last_compute(ctx->device))
+    FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, prev, 0));
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
   // the NE pass converts the ELL payloads to weights itself when it can
   const bool fuse_w = !reuse && cached_q < 0 && !w64 && bits <= 15 && ctx->ne_variant == 1;
@@ -639,8 +662,9 @@ static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coord
     }
   }
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
-  FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_side, ctx->stream));
-  FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_side));
+  FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
+  device_last_compute(ctx->device) = ctx->ev_done;
+  if (!ctx->async_lock || cached_q < 0 || slab) FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_done));
   compute_lock.unlock();
   if (!dev && (rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), false))) return rc;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));

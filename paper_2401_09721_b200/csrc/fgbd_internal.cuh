@@ -151,6 +151,8 @@ struct fgbd_ctx {
   const uint32_t* rowid = nullptr;  // row -> point (line-1 perm) when reordered
   int* pos = nullptr;             // point -> row (cap)
   cudaEvent_t ev_perm = nullptr;  // line-1 permutation ready (main stream)
+  cudaEvent_t ev_done = nullptr;  // this context's last frame compute finished
+  int async_lock = 1;             // FGBD_ASYNC_LOCK: order frames on the GPU, not the host
   // static-geometry reuse (FGBD_FLAG_REUSE_GRAPH): coordinates and header of
   // the held graph
   int64_t* held_coords = nullptr;  // 3 x held_cap int64

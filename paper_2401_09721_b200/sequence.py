@@ -76,7 +76,7 @@ def _run_many(fn, items, workers):
 
 def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
                      cfg: FilterConfig = FilterConfig(), *, n_frames: int | None = None,
-                     workers: int = 2, process_group=None, denoise_fn=None,
+                     workers: int = 3, process_group=None, denoise_fn=None,
                      sink: Callable[[int, PointCloud, DenoiseReport], object] | None = None,
                      reuse_graph: bool = True,
                      ) -> dict[int, tuple[PointCloud, DenoiseReport]]:
