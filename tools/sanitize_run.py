@@ -1,6 +1,7 @@
-"""Small end-to-end workload touching every device entry point (a sanitizer-style
-synccheck): one select frame, one cached frame, a reused-graph frame, PLY,
-kNN, quantize, psnr and the device noise generator, on small clouds."""
+"""Small end-to-end workload touching every device entry point: a select
+frame, a cached frame and a reused-graph frame per cloud kind, PLY, kNN,
+psnr and the device noise generator, on small clouds.  Written for
+compute-sanitizer, which this GPU pool does not allow, so it runs plain."""
 import sys
 from pathlib import Path
 
