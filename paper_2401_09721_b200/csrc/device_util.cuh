@@ -1,5 +1,6 @@
 // Small device helpers: warp/block reductions, lane masks, last-block tickets.
 #pragma once
+#include <cstdio>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -13,6 +14,27 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
+
+// Device-side bounds checks for debug builds (-DFGBD_DEBUG_BOUNDS=1, used by
+// tools/debug_bounds.sh in place of compute-sanitizer): a failed check
+// prints its site and traps, so the call fails loudly.
+#ifndef FGBD_DEBUG_BOUNDS
+#define FGBD_DEBUG_BOUNDS 0
+#endif
+#if FGBD_DEBUG_BOUNDS
+#define FGBD_DCHECK(cond)                                                           \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("FGBD_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+             #cond, (int)blockIdx.x, (int)threadIdx.x);                             \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define FGBD_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

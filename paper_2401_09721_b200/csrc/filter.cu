@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kBlock) k_expand(const double* __restrict__ sr
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int64_t p = rowid ? (int64_t)rowid[i] : i;
+    FGBD_DCHECK(p >= 0 && p < n);
     st_row(dst + i, make_double4(src[3 * p], src[3 * p + 1], src[3 * p + 2], 0.0));
   }
 }
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(kBlock) k_compact(double* const* bufs, const C
   const double4* s = src ? src : reinterpret_cast<const double4*>(bufs[ctl->best_buf]);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    FGBD_DCHECK(!pos || (pos[i] >= 0 && pos[i] < n));
     const double4 v = ld_row(s + (pos ? (int64_t)pos[i] : i));  // point i lives in row pos[i]
     if (CLIP) {
       dst[3 * i] = fmin(fmax(v.x, 0.0), 255.0);
@@ -494,6 +496,10 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
       }
       if (inext < end) load_row_slots<WM>(a, inext, pol_stream, neg_inv_sg2, nbn, wn);
     }
+#if FGBD_DEBUG_BOUNDS
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) FGBD_DCHECK(ell_j(nbc[s]) < n);
+#endif
     if (FGBD_LF_PF && i + FGBD_LF_PFD * stride < end)
 #pragma unroll
       for (int s = 0; s < kSlots; s += 2)

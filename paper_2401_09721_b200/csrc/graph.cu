@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
       sq[s] = ~0ull;
       if (s < deg) {
         long long xj, yj, zj;
+        FGBD_DCHECK((int64_t)c[s] < n);
         unpack(pc[c[s]], b, &xj, &yj, &zj);
         const long long dx = xi - xj, dy = yi - yj, dz = zi - zj;
         sq[s] = (unsigned long long)(dx * dx + dy * dy + dz * dz);

@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kNe2Warps * 32, 6) k_noise2(const uint32_t* __
           int j = nb[0];
 #pragma unroll
           for (int t = 1; t < kSlots; ++t) j = (s == t) ? nb[t] : j;
+          FGBD_DCHECK(j >= 0 && j < n);
           v[r] = ld_row(colors + j);
         }
       }

@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
 #pragma unroll
         for (int s = 0; s < kSlots; ++s) {
           const int64_t j = ell_j(nb[s]);
+          FGBD_DCHECK(j >= 0 && j < a.n);
           const double4* src =
               (j >= lo && j < hi) ? own_in : a.bufs[owner_of(a, j)][ib];  // halo: peer memory
           gv[s] = ld_row_hint(src + j, pol_keep);

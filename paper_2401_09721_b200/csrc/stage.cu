@@ -29,6 +29,7 @@ __global__ void k_extract(const uint32_t* __restrict__ meta, const int* __restri
     const uint32_t mt = meta[i];
     if ((int)(mt & 7u) < D - 1) continue;
     const int64_t p = pos[i];
+    FGBD_DCHECK(p >= 0 && p < ne);
     if (pidx) pidx[p] = i;
     if (!vec) continue;
     for (int c = 0; c < 3; ++c) vec[((int64_t)c * ne + p) * D] = colors[4 * i + c];
