@@ -154,7 +154,10 @@ __device__ __forceinline__ double patch_std(const double4 (&v)[7], int c, int D,
 }
 
 template <bool WEIGHTS>
-__global__ void __launch_bounds__(kNe2Warps * 32, 6) k_noise2(const uint32_t* __restrict__ meta,
+#ifndef FGBD_NE_MINB
+#define FGBD_NE_MINB 6
+#endif
+__global__ void __launch_bounds__(kNe2Warps * 32, FGBD_NE_MINB) k_noise2(const uint32_t* __restrict__ meta,
                                                            EllRef ell,
                                                            const double4* __restrict__ colors,
                                                            int64_t n, int D,
