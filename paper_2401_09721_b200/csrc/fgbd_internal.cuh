@@ -116,14 +116,14 @@ struct fgbd_ctx {
   double* out = nullptr;        // (N,3) fp64 result staging
   double* fslr = nullptr;       // [N]
   uint32_t* mask = nullptr;     // [ceil(N/32)]
-  double* partials = nullptr;   // reduction partials (1<<17 doubles)
+  double* partials = nullptr;   // reduction partials (>= 1<<19 doubles)
   unsigned int* tickets = nullptr;  // group tickets for hierarchical reductions
   int lf_variant = 10;          // filter-step kernel (FGBD_LF_VARIANT): 0 per-step, 2+ persistent
-  int coop_blocks[64] = {};      // co-resident grid of each persistent instantiation
-  int lf_shape = 0;
-  int lf_halo = 128;  // FGBD_LF_HALO: window rows either side of a TMA tile
-  int lf_chunk = 1;
-  int reorder_rows = 1;  // FGBD_REORDER: denoise-path rows in scan-line-1 order  // FGBD_LF_CHUNK: contiguous row range per block (0 = grid-stride)             // persistent kernel block shape (FGBD_LF_SHAPE)
+  int coop_blocks[64] = {};     // co-resident grid of each persistent instantiation
+  int lf_shape = 0;             // persistent kernel block shape (FGBD_LF_SHAPE)
+  int lf_halo = 128;            // FGBD_LF_HALO: window rows either side of a TMA tile
+  int lf_chunk = 1;             // FGBD_LF_CHUNK: contiguous row range per block (0 = grid-stride)
+  int reorder_rows = 1;         // FGBD_REORDER: denoise-path rows in scan-line-1 order
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)
