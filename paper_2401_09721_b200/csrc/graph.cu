@@ -2,7 +2,6 @@
 //
 //   k_prep       coords int64 -> packed line-1 code (pc) + digit histograms
 //                of all three scan lines for every radix pass (one read)
-//   k_scan_hist  histograms -> exclusive digit bases
 //   k_onesweep   one stable LSD pass for all three lines: warp multisplit
 //                (per-bit ballots) -> decoupled look-back across tiles -> smem
 //                reorder -> coalesced scatter (8-bit digits, ceil(3b/8)
@@ -108,27 +107,6 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
     if (s_hist[t]) atomicAdd(&hist[t], s_hist[t]);
 }
 
-// Exclusive scan of each 256-bin histogram, in place.  One block of 256.
-__global__ void k_scan_hist(uint32_t* hist, int nhist) {
-  __shared__ uint32_t s_w[8];
-  const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
-  for (int h = 0; h < nhist; ++h) {
-    const uint32_t c = hist[h * kRadix + d];
-    uint32_t v = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, v, o);
-      if (lane >= o) v += t;
-    }
-    if (lane == 31) s_w[warp] = v;
-    __syncthreads();
-    uint32_t off = 0;
-    for (int w = 0; w < warp; ++w) off += s_w[w];
-    hist[h * kRadix + d] = off + v - c;
-    __syncthreads();
-  }
-}
-
 // ---------------------------------------------------------------------------
 // onesweep pass
 // ---------------------------------------------------------------------------
@@ -139,7 +117,7 @@ struct SortPass {
   const uint32_t* src_vals[3];  // null on pass 0 (identity)
   void* dst_keys[3];
   uint32_t* dst_vals[3];
-  const uint32_t* bases;        // [line][passes][256]
+  const uint32_t* hist;         // [line][passes][256] digit counts (k_prep)
   unsigned long long* status;   // [line][tiles][256]
   unsigned int* tile_ctr;       // [line]
   int64_t n;
@@ -180,7 +158,7 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   uint32_t* s_whist = s_vals + kSortTile;  // [8 warps][256]
   __shared__ uint32_t s_start[kRadix];    // tile-local exclusive digit start
   __shared__ uint32_t s_gofs[kRadix];     // global position - local index
-  __shared__ uint32_t s_wsum[8];
+  __shared__ uint32_t s_wsum[8], s_hsum[8];
   __shared__ int s_tile;
 
   const int line = blockIdx.y;
@@ -257,6 +235,8 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
     count += c;
   }
   STLOG(1);
+  // this digit's count over the whole pass (its latency hides in the look-back)
+  const uint32_t hcount = p.hist[(line * p.passes + p.pass) * kRadix + d];
   // decoupled look-back over preceding tiles of this line
   unsigned long long* st = p.status + ((int64_t)line * p.tiles) * kRadix;
   const unsigned long long ep = (unsigned long long)p.epoch << 34;
@@ -291,20 +271,31 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
     atomicExch(&st[(int64_t)tile * kRadix + d], ep | kFlagPre | (excl + count));
   }
   // tile-local exclusive scan of counts over digits
-  uint32_t v = count;
+  // and the pass's global digit base: the same scan over k_prep's histogram
+  uint32_t v = count, hv = hcount;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t t = __shfl_up_sync(kFull, v, o);
-    if (lane >= o) v += t;
+    const uint32_t th = __shfl_up_sync(kFull, hv, o);
+    if (lane >= o) {
+      v += t;
+      hv += th;
+    }
   }
-  if (lane == 31) s_wsum[warp] = v;
+  if (lane == 31) {
+    s_wsum[warp] = v;
+    s_hsum[warp] = hv;
+  }
   __syncthreads();
-  uint32_t wofs = 0;
+  uint32_t wofs = 0, hofs = 0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) wofs += (w < warp) ? s_wsum[w] : 0u;
+  for (int w = 0; w < 8; ++w) {
+    wofs += (w < warp) ? s_wsum[w] : 0u;
+    hofs += (w < warp) ? s_hsum[w] : 0u;
+  }
   const uint32_t start = wofs + v - count;
   s_start[d] = start;
-  s_gofs[d] = p.bases[(line * p.passes + p.pass) * kRadix + d] + excl - start;
+  s_gofs[d] = (hofs + hv - hcount) + excl - start;
   __syncthreads();
   STLOG(2);  // every digit's look-back is done
   // reorder the tile in shared memory by digit (stable)
@@ -746,7 +737,7 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
     }
     FGBD_LAUNCH(ctx);
   }
-  k_scan_hist<<<1, kRadix, 0, ctx->stream>>>(S.hist, nlines * passes);
+
   FGBD_LAUNCH(ctx);
   for (int pass = 0; pass < passes; ++pass) {
     SortPass p{};
@@ -757,7 +748,7 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
       p.dst_vals[l] = S.vals[pass & 1][l];
     }
     p.pc = ctx->pc;
-    p.bases = S.hist;
+    p.hist = S.hist;
     p.status = S.status;
     p.tile_ctr = S.tile_ctr + pass * 3;
     p.n = n;
