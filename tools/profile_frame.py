@@ -2,7 +2,7 @@
 
     python tools/profile_frame.py [--kind ramp] [--n 1000000] [--frames 3]
 
-Launch order per frame (config 2, ramp, b=7): memset x2, k_prep, k_scan_hist,
+Launch order per frame (config 2, ramp, b=7): memset x2, k_prep,
 3 x k_onesweep, k_neighbors, k_rows, k_weights, k_noise, k_reduce_cols,
 k_mask, 64 x k_lf_step, k_finalize.
 """
