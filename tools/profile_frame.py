@@ -2,9 +2,9 @@
 
     python tools/profile_frame.py [--kind ramp] [--n 1000000] [--frames 3]
 
-Launch order per frame (config 2, ramp, b=7): memset x2, k_prep,
-3 x k_onesweep, k_neighbors, k_rows, k_weights, k_noise, k_reduce_cols,
-k_mask, 64 x k_lf_step, k_finalize.
+Launch order per frame (config 2, ramp, b=7): k_prep, 3 x k_onesweep,
+k_neighbors, k_rows, k_expand (side stream), k_noise2 (weights fused),
+k_reduce_cols, k_mask, k_lf_run (all S steps), k_compact.
 """
 
 from __future__ import annotations
