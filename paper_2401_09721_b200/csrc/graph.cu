@@ -737,8 +737,6 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
     }
     FGBD_LAUNCH(ctx);
   }
-
-  FGBD_LAUNCH(ctx);
   for (int pass = 0; pass < passes; ++pass) {
     SortPass p{};
     for (int l = 0; l < nlines; ++l) {
