@@ -67,9 +67,28 @@ def parse():
     return ap.parse_args()
 
 
+# FGBD_BENCH_SHARED_GPU=1 is a harness check only: every rank runs on GPU 0
+# and the ranks meet over gloo, so the N>1 code path (barriers, max over
+# ranks, whole-job value) can be exercised on a one-GPU box.  The ranks'
+# frames are independent, so no kernel waits on another rank.  Its numbers
+# are not bench values (the ranks share one GPU).
+SHARED_GPU = os.environ.get("FGBD_BENCH_SHARED_GPU") == "1"
+
+
 def dist_env():
+    local = int(os.environ.get("LOCAL_RANK", 0))
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
-            int(os.environ.get("LOCAL_RANK", 0)))
+            0 if SHARED_GPU else local)
+
+
+def init_dist(local):
+    import torch
+    import torch.distributed as dist
+
+    if SHARED_GPU:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
 
 def make_frame(kind, n, sigma, seed):
@@ -87,6 +106,8 @@ def config_block(args, world, extra=None):
          "l2": "flushed between timed steps (256 MiB write, untimed)"}
     if extra:
         c.update(extra)
+    if SHARED_GPU:
+        c["harness_check"] = "FGBD_BENCH_SHARED_GPU: all ranks on GPU 0 over gloo; not a bench value"
     return c
 
 
@@ -175,7 +196,7 @@ def run_b200(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     clean, noisy = make_frame(args.kind, args.n, args.sigma, seed=1 + rank)
     n = noisy.n_points
     ctx = nat.context()
@@ -428,7 +449,7 @@ def run_video(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
         pg = dist.group.WORLD
     # a pool of distinct noisy frames in pinned memory, cycled over the video
     clean, _ = fb.generate_cloud(args.kind, args.n, seed=0)
@@ -515,7 +536,7 @@ def run_ply(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
         pg = dist.group.WORLD
     # distinct noisy frames serialised as binary PLY files held in pinned memory
     clean, _ = fb.generate_cloud(args.kind, args.n, seed=0)
@@ -598,7 +619,7 @@ def run_slab(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
         pg = dist.group.WORLD
     n = args.n if args.n != N_POINTS else 8_000_000
     clean, _ = fb.generate_cloud(args.kind, n, seed=0)
