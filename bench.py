@@ -47,12 +47,14 @@ L2_FLUSH_BYTES = 256 << 20
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="ranks (one per GPU); without torchrun, N > 1 re-launches this "
+                         "script under torch.distributed.run (default: WORLD_SIZE or 1)")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--kind", default=KIND)
-    ap.add_argument("--n", type=int, default=N_POINTS)
+    ap.add_argument("--points", "--n", dest="n", type=int, default=N_POINTS)
     ap.add_argument("--sigma", type=float, default=SIGMA)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -75,6 +77,38 @@ def parse():
 SHARED_GPU = os.environ.get("FGBD_BENCH_SHARED_GPU") == "1"
 
 
+def launch_plan(gpus, env, argv):
+    """How to honour `--gpus`: ("run", world) when this process is (one rank
+    of) the job, ("relaunch", cmd) when N > 1 ranks must be started first.
+
+    The driver starts N > 1 under torchrun (WORLD_SIZE set); a plain
+    `python bench.py --gpus N` starts the ranks itself, so the N it prints is
+    the N that ran.  A mismatch between --gpus and WORLD_SIZE is an error.
+    """
+    ws = env.get("WORLD_SIZE")
+    if ws is not None:
+        world = int(ws)
+        if gpus is not None and gpus != world:
+            raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}")
+        return "run", world
+    world = 1 if gpus is None else int(gpus)
+    if world < 1:
+        raise SystemExit(f"bench.py: --gpus must be >= 1, got {world}")
+    if world == 1:
+        return "run", 1
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()),
+           # torchrun's parser takes "--n" for an abbreviation of its own options
+           *[("--points" + a[3:]) if a == "--n" or a.startswith("--n=") else a for a in argv]]
+    return "relaunch", cmd
+
+
 def dist_env():
     local = int(os.environ.get("LOCAL_RANK", 0))
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
@@ -91,6 +125,11 @@ def init_dist(local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
 
+def warmup_steps(args):
+    """W >= 3 untimed warm-up steps, the same count in both arms."""
+    return max(args.warmup, 3)
+
+
 def make_frame(kind, n, sigma, seed):
     import paper_2401_09721_b200 as fb
 
@@ -98,14 +137,13 @@ def make_frame(kind, n, sigma, seed):
     return clean, fb.add_gaussian_noise(clean, sigma, seed=seed)
 
 
-def config_block(args, world, extra=None):
+def config_block(args, world):
+    """Identical in both arms (the driver compares them key for key)."""
     c = {"workload": f"single {args.n:,}-point synthetic '{args.kind}' frame, sigma={args.sigma:g}, "
                      "default FilterConfig (BASELINE.json configs[1])",
          "n_points": args.n, "kind": args.kind, "sigma": args.sigma,
          "parallelism": f"frame-parallel x{world}" if world > 1 else "single GPU",
          "l2": "flushed between timed steps (256 MiB write, untimed)"}
-    if extra:
-        c.update(extra)
     if SHARED_GPU:
         c["harness_check"] = "FGBD_BENCH_SHARED_GPU: all ranks on GPU 0 over gloo; not a bench value"
     return c
@@ -224,7 +262,7 @@ def run_b200(args):
         torch.cuda.synchronize()
 
     clk = Clocks(local).__enter__()
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(warmup_steps(args)):
         step_device()
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -273,7 +311,7 @@ def run_b200(args):
     clocks = clk.summary()
 
     # e2e: public API, pinned host inputs, H2D + D2H inside each step
-    e2e = None
+    e2e = e2e_pageable = None
     if not args.no_e2e:
         pc_coords = nat.pinned_empty(noisy.coords.shape, np.int64)
         pc_coords[...] = noisy.coords
@@ -281,8 +319,8 @@ def run_b200(args):
         pc_colors[...] = noisy.colors
         pc = fb.PointCloud(pc_coords, pc_colors, noisy.bit_depth)
         assert pc.coords.ctypes.data == pc_coords.ctypes.data
-        for _ in range(max(args.warmup, 3)):  # same shape as the timed loop: the
-            out, rep = fb.denoise(pc)          # pinned output pool reaches steady state
+        for _ in range(warmup_steps(args)):  # same shape as the timed loop: the
+            out, rep = fb.denoise(pc)         # pinned output pool reaches steady state
         barrier()
         t_e2e, dev_t = [], []
         for k in range(args.steps):
@@ -311,6 +349,33 @@ def run_b200(args):
                                 "coords_h2d": 1e3 * float(np.mean([d[1] for d in dev_t])),
                                 "colors_d2h": 1e3 * float(np.mean([d[2] for d in dev_t]))},
                "path": "paper_2401_09721_b200.denoise(PointCloud) -> fgbd_denoise C-ABI, pinned host inputs"}
+        # the same with ordinary (pageable) NumPy inputs, as load_ply /
+        # add_gaussian_noise hand them over
+        pg_pc = fb.PointCloud(np.array(noisy.coords), np.array(noisy.colors), noisy.bit_depth)
+        for _ in range(warmup_steps(args)):
+            fb.denoise(pg_pc)
+        barrier()
+        t_pg = []
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out, rep = fb.denoise(pg_pc)
+            t_pg.append(time.perf_counter() - t0)
+        barrier()
+        pg_s = float(sum(t_pg))
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([pg_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pg_s = float(t.item())
+        e2e_pageable = {"value": world * args.steps / pg_s, "unit": "frames/s",
+                        "h2d_bytes_per_step": int(pg_pc.coords.nbytes + pg_pc.colors.nbytes),
+                        "d2h_bytes_per_step": int(out.colors.nbytes),
+                        "ms_per_step": 1e3 * pg_s / args.steps,
+                        "path": "paper_2401_09721_b200.denoise(PointCloud) with pageable NumPy inputs"}
 
 
     # CPU baseline + parity spot check (rank 0, N = 1 only)
@@ -341,12 +406,12 @@ def run_b200(args):
         ms = total_ms / args.steps
         line = {
             "metric": METRIC, "value": world * args.steps / (total_ms / 1e3), "unit": "frames/s",
-            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "n_gpus": world, "steps": args.steps, "warmup": warmup_steps(args),
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(args, world, {"bit_depth": int(noisy.bit_depth),
-                                                 "selected_q": q, "filter_steps_S": S,
-                                                 "n_edges": int(rep0.n_edges)}),
+            "config": config_block(args, world),
+            "frame": {"bit_depth": int(noisy.bit_depth), "selected_q": q, "filter_steps_S": S,
+                      "n_edges": int(rep0.n_edges)},
             "mpoints_per_s": world * args.steps * n / (total_ms / 1e3) / 1e6,
             "stage_ms": stage,
             "roofline": {"bound": "hbm", "kernel": "k_lf_run",
@@ -363,7 +428,8 @@ def run_b200(args):
                 "unit": "GB/s",
                 "frac": frame_bytes / (total_ms / args.steps / 1e3) / 1e9 / peak,
                 "roofline_fps": peak * 1e9 / frame_bytes},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable,
+            "gpu_launches": launches, "clocks": clocks,
             "parity": parity,
         }
         print(json.dumps(line), flush=True)
@@ -401,7 +467,7 @@ def run_reference(args):
     os.environ["OMP_NUM_THREADS"] = "1"
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     ctx = mp.get_context("spawn")
-    warm = min(args.warmup, 1)
+    warm = warmup_steps(args)
     walls, qs = [], set()
     with ctx.Pool(procs) as pool:
         for k in range(warm + args.steps):
@@ -676,6 +742,10 @@ def run_slab(args):
 
 def main():
     args = parse()
+    what, plan = launch_plan(args.gpus, os.environ, sys.argv[1:])
+    if what == "relaunch":
+        sys.exit(subprocess.call(plan))
+    args.gpus = plan
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "video":

@@ -113,6 +113,12 @@ typedef struct fgbd_report {
   double t_h2d;                /* coordinates host->device (colours overlap the graph build) */
   double t_d2h;                /* denoised colours device->host */
   int32_t graph_reused;        /* 1: FGBD_FLAG_REUSE_GRAPH matched the held graph */
+  /* per channel: 1 when Jacobi's difference-of-sums convergence test
+     (noise.py:152) never met its target but the directly summed
+     off-diagonal norm did -- the reference raises NoiseEstimationError
+     "Jacobi did not converge" on such a matrix (noise.py:180-185); this
+     build returns the eigenvalues */
+  int32_t jacobi_direct_off[3];
 } fgbd_report;
 
 /* Result of NE-GBP (noise.py:63-73). */
@@ -126,6 +132,7 @@ typedef struct fgbd_noise {
   int32_t fallback[3];
   int64_t eligible_count;
   int32_t patch_size;
+  int32_t jacobi_direct_off[3]; /* see fgbd_report.jacobi_direct_off */
 } fgbd_noise;
 
 /* Shape of the graph held by a context after fgbd_build_graph. */
@@ -241,6 +248,11 @@ int32_t fgbd_edge_weights(fgbd_ctx* ctx, const double* edge_sqdist, int64_t n_ed
 /* symmetric_eigenvalues (noise.py:133-185), host C++ Jacobi. */
 int32_t fgbd_symmetric_eigenvalues(const double* s, int32_t d, double* out_desc,
                                    char* err, int32_t err_len);
+/* The same, also reporting in *direct_off whether the result was accepted
+ * only by the directly summed off-diagonal norm -- i.e. the reference would
+ * have raised "Jacobi did not converge" (noise.py:180-185). */
+int32_t fgbd_symmetric_eigenvalues_ex(const double* s, int32_t d, double* out_desc,
+                                      int32_t* direct_off, char* err, int32_t err_len);
 /* select_tail (noise.py:188-216). */
 int32_t fgbd_select_tail(const double* lam, int32_t d, int32_t tau_divisor,
                          int32_t* m, double* tau, int32_t* fallback,

@@ -55,7 +55,7 @@ class Report(C.Structure):
                 ("tail_tau", c_f64 * 3), ("tail_fallback", c_i32 * 3), ("n_trace", c_i32),
                 ("trace", c_f64 * TRACE_MAX), ("gpu_launches", c_i32),
                 ("t_lf_steps", c_f64), ("t_h2d", c_f64), ("t_d2h", c_f64),
-                ("graph_reused", c_i32)]
+                ("graph_reused", c_i32), ("jacobi_direct_off", c_i32 * 3)]
 
 
 class Noise(C.Structure):
@@ -63,7 +63,8 @@ class Noise(C.Structure):
                 ("eigenvalues", (c_f64 * MAX_PATCH) * 3),
                 ("covariance", ((c_f64 * MAX_PATCH) * MAX_PATCH) * 3),
                 ("m", c_i32 * 3), ("tau", c_f64 * 3), ("fallback", c_i32 * 3),
-                ("eligible_count", c_i64), ("patch_size", c_i32)]
+                ("eligible_count", c_i64), ("patch_size", c_i32),
+                ("jacobi_direct_off", c_i32 * 3)]
 
 
 class GraphInfo(C.Structure):
@@ -100,6 +101,8 @@ _SIGNATURES = {
     "fgbd_edge_weights": (c_i32, [C.c_void_p, C.c_void_p, c_i64, c_f64, P(c_f64), C.c_void_p,
                                   c_u32]),
     "fgbd_symmetric_eigenvalues": (c_i32, [C.c_void_p, c_i32, C.c_void_p, C.c_char_p, c_i32]),
+    "fgbd_symmetric_eigenvalues_ex": (c_i32, [C.c_void_p, c_i32, C.c_void_p, C.c_void_p,
+                                              C.c_char_p, c_i32]),
     "fgbd_select_tail": (c_i32, [C.c_void_p, c_i32, c_i32, P(c_i32), P(c_f64), P(c_i32),
                                  C.c_char_p, c_i32]),
     "fgbd_slab_create": (C.c_void_p, [C.c_void_p, c_i32, c_i32, c_i64, c_i32]),

@@ -365,6 +365,7 @@ void fill_noise_report(fgbd_report* r, const fgbd_noise& nz) {
     r->tail_tau[c] = nz.tau[c];
     r->tail_fallback[c] = nz.fallback[c];
     for (int k = 0; k < FGBD_MAX_PATCH; ++k) r->eigenvalues[c][k] = nz.eigenvalues[c][k];
+    r->jacobi_direct_off[c] = nz.jacobi_direct_off[c];
   }
   r->eligible_count = nz.eligible_count;
 }
@@ -553,8 +554,12 @@ static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coord
   const int w64 = (flags & FGBD_FLAG_WEIGHTS_F64) ? 1 : 0;
   if (n < 2) {  // filtering.py:269-275: the input comes back unchanged
     if (n > 0 && out_colors != colors) {
-      if ((rc = d2h(ctx, out_colors, colors, 3 * n * sizeof(double), dev))) return rc;
-      FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      if (dev) {
+        if ((rc = d2h(ctx, out_colors, colors, 3 * n * sizeof(double), true))) return rc;
+        FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      } else {
+        std::memcpy(out_colors, colors, 3 * n * sizeof(double));
+      }
     }
     return FGBD_OK;
   }
@@ -1080,7 +1085,18 @@ int32_t fgbd_symmetric_eigenvalues(const double* s, int32_t d, double* out_desc,
                                    int32_t err_len) {
   std::string msg;
   if (d < 1) msg = "matrix must be square";
-  int rc = d < 1 ? FGBD_E_NOISE : jacobi_eigenvalues(s, d, out_desc, &msg);
+  int rc = d < 1 ? FGBD_E_NOISE : jacobi_eigenvalues(s, d, out_desc, &msg, nullptr);
+  if (rc && err && err_len > 0) std::snprintf(err, err_len, "%s", msg.c_str());
+  return rc;
+}
+
+int32_t fgbd_symmetric_eigenvalues_ex(const double* s, int32_t d, double* out_desc,
+                                      int32_t* direct_off, char* err, int32_t err_len) {
+  std::string msg;
+  int flag = 0;
+  if (d < 1) msg = "matrix must be square";
+  int rc = d < 1 ? FGBD_E_NOISE : jacobi_eigenvalues(s, d, out_desc, &msg, &flag);
+  if (direct_off) *direct_off = flag;
   if (rc && err && err_len > 0) std::snprintf(err, err_len, "%s", msg.c_str());
   return rc;
 }

@@ -228,7 +228,8 @@ int scan_exclusive(fgbd_ctx* ctx, const int64_t* in, int64_t n, int64_t* out, in
 int launch_noise(fgbd_ctx* ctx, int64_t n, int patch, int fuse_weights);
 // host side: covariance -> Jacobi -> tail -> sigma (noise.py:122-243)
 int finish_noise(fgbd_ctx* ctx, int patch, int divisor, fgbd_noise* out);
-int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err);
+int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err,
+                       int* direct_off);
 int select_tail_host(const double* lam, int d, int divisor, int* m, double* tau,
                      int* fallback, std::string* err);
 

@@ -327,7 +327,9 @@ static double np_pairwise_sum(const double* x, int n) {
   return res;
 }
 
-int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err) {
+int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err,
+                       int* direct_off) {
+  if (direct_off) *direct_off = 0;
   // symmetry check on the raw input (noise.py:142-144)
   double scale = 0.0, asym = 0.0;
   for (int i = 0; i < d * d; ++i) scale = std::max(scale, std::fabs(s[i]));
@@ -421,6 +423,8 @@ int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* er
     for (int q = 0; q < d; ++q)
       if (p != q) off_direct += a[p * d + q] * a[p * d + q];
   if (off <= target || std::sqrt(off_direct) <= target) {
+    // the reference would have raised here (noise.py:180-185): say so
+    if (direct_off && !(off <= target)) *direct_off = 1;
     finish();
     return FGBD_OK;
   }
@@ -505,7 +509,7 @@ int finish_noise(fgbd_ctx* ctx, int D, int divisor, fgbd_noise* out) {
       for (int l = 0; l < D; ++l) out->covariance[c][k][l] = cov[k * D + l];
     std::string err;
     double lam[7];
-    int rc = jacobi_eigenvalues(cov, D, lam, &err);
+    int rc = jacobi_eigenvalues(cov, D, lam, &err, &out->jacobi_direct_off[c]);
     if (rc) return set_error(ctx, rc, err);
     int m, fb;
     double tau;

@@ -53,7 +53,7 @@ struct SlabArgs {
   double* part;           // local [groups][bpg][4] block partials
   const uint32_t* mask;
   Ctl* ctl;               // local control block (state + trace)
-  unsigned long long epoch;  // frame epoch: counters are epoch*4096 + step
+  unsigned long long epoch;  // frame epoch: counters are epoch<<32 | step
   int fixed_steps;        // cached path when > 0 (no criterion)
   int select;
 };
@@ -68,7 +68,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 }
 
 // Barrier over the bpg co-resident blocks of one group (sense-reversing).
-__device__ __forceinline__ void group_barrier(unsigned int* bar, int nblocks) {
+__device__ __forceinline__ void group_barrier(unsigned int* bar, int nblocks, Ctl* ctl) {
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned int* gen = bar + 1;
@@ -81,7 +81,10 @@ __device__ __forceinline__ void group_barrier(unsigned int* bar, int nblocks) {
     } else {
       const long long t0 = clock64();
       while (*gen == g0) {
-        if (clock64() - t0 > (1ll << 35)) break;  // ~17 s: never hang the GPU
+        if (clock64() - t0 > (1ll << 35)) {  // ~17 s: never hang the GPU; report it
+          atomicOr(&ctl->err_flags, 4);
+          break;
+        }
       }
     }
     __threadfence();
@@ -227,9 +230,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
     double* part = a.part + ((int64_t)g * a.bpg + lb) * 4;
     if (threadIdx.x == 0)
       for (int k = 0; k < 3; ++k) part[k] = sx[k];
-    group_barrier(gbar, a.bpg);  // this rank's rows of step q+1 are written
+    group_barrier(gbar, a.bpg, ctl);  // this rank's rows of step q+1 are written
     const int par = (q + 1) & 1;
-    const unsigned long long tick = a.epoch * 4096ull + (unsigned long long)(q + 1);
+    const unsigned long long tick = (a.epoch << 32) | (unsigned long long)(q + 1);
     if (lb == 0 && threadIdx.x == 0) {
       double t[3] = {0.0, 0.0, 0.0};
       for (int b = 0; b < a.bpg; ++b)
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
           }
         }
     }
-    group_barrier(gbar, a.bpg);  // every rank's rows and totals of step q+1 are visible
+    group_barrier(gbar, a.bpg, ctl);  // every rank's rows and totals of step q+1 are visible
     if (threadIdx.x == 0) {
       if (a.select) {
         double tot[3] = {0.0, 0.0, 0.0};

@@ -249,6 +249,10 @@ def _device_info(r: nat.Report, patch: int) -> dict:
         "t_h2d": float(r.t_h2d),
         "t_d2h": float(r.t_d2h),
         "graph_reused": bool(r.graph_reused),
+        # True per channel where the reference would have raised "Jacobi did
+        # not converge" (noise.py:180-185) and this build returned the
+        # eigenvalues instead
+        "jacobi_direct_off": [bool(v) for v in r.jacobi_direct_off],
     }
 
 
@@ -284,11 +288,11 @@ def denoise_frame(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
     rep = nat.Report()
     cq = -1 if cached_q is None else int(cached_q)
     cs = float("nan") if cached_sigma_est is None else float(cached_sigma_est)
+    ctx.graph_token = None  # the call rebuilds the device graph, even when it fails
     ctx.check(ctx.lib.fgbd_denoise(ctx.handle, nat.ptr(pc_noisy.coords), nat.ptr(pc_noisy.colors),
                                    n, bits, nat.make_config(cfg), cq, cs, nat.ptr(out), rep,
                                    nat.FLAG_REUSE_GRAPH if reuse_graph else 0),
               "denoise")
-    ctx.graph_token = None
     report = _report_from(rep, cfg, cached_q, cached_sigma_est)
     out.flags.writeable = False
     return PointCloud._trusted(pc_noisy.coords, out, pc_noisy.bit_depth), report

@@ -124,9 +124,9 @@ def scanline_codes(pc: PointCloud, line: int) -> ScanLineCodes:
     ctx = nat.context()
     n = pc.n_points
     codes = np.empty(n, np.uint64)
+    ctx.graph_token = None  # the sort scratch is shared with the held SLG
     ctx.check(ctx.lib.fgbd_scan_line(ctx.handle, nat.ptr(pc.coords), n, b, line,
                                      nat.ptr(codes), None, 0), "scanline_codes")
-    ctx.graph_token = None
     return ScanLineCodes(codes, line, b)
 
 
@@ -140,9 +140,9 @@ def radix_argsort(keys: np.ndarray, key_bits: int = 64) -> np.ndarray:
         return np.arange(n, dtype=np.int64)
     ctx = nat.context()
     perm = np.empty(n, np.int64)
+    ctx.graph_token = None  # the sort scratch is shared with the held SLG
     ctx.check(ctx.lib.fgbd_radix_argsort(ctx.handle, nat.ptr(keys), n, int(key_bits),
                                          nat.ptr(perm), 0), "radix_argsort")
-    ctx.graph_token = None
     return perm
 
 
@@ -154,6 +154,7 @@ def sort_permutation(codes: ScanLineCodes) -> np.ndarray:
 def _device_build(pc: PointCloud, weights64: bool = False) -> tuple[nat.Context, object]:
     b = _require_quantized(pc)
     ctx = nat.context()
+    ctx.graph_token = None
     info = nat.GraphInfo()
     flags = nat.FLAG_WEIGHTS_F64 if weights64 else 0
     ctx.check(ctx.lib.fgbd_build_graph(ctx.handle, nat.ptr(pc.coords), pc.n_points, b,
@@ -237,6 +238,7 @@ def ensure_device_graph(pc: PointCloud, g: Graph | None, weights64: bool = False
         return ctx
     if g is not None and g.n != pc.n_points:
         raise GraphError(f"graph has {g.n} vertices for a {pc.n_points}-point cloud")
+    ctx.graph_token = None  # a failed rebuild leaves no valid graph behind
     ctx, info = _device_build(pc, weights64)
     if g is not None and not g._slg:
         _check_is_slg(ctx, info, g)
@@ -273,10 +275,10 @@ def build_knn_brute(pc: PointCloud, k: int) -> Graph:
     ctx = nat.context()
     e = nat.c_i64()
     q = pc.is_quantized
+    ctx.graph_token = None  # the sort scratch was shared with the held SLG
     ctx.check(ctx.lib.fgbd_knn_build(ctx.handle, nat.ptr(pc.coords) if q else None,
                                      None if q else nat.ptr(pc.coords), n, k,
                                      int(pc.bit_depth) if q else 0, e, 0), "build_knn_brute")
-    ctx.graph_token = None  # the sort scratch was shared with the held SLG
     m = int(e.value)
     indptr = np.empty(n + 1, np.int64)
     indices = np.empty(2 * m, np.int64)

@@ -96,6 +96,9 @@ class NoiseEstimate:
     tau: np.ndarray
     fallback: np.ndarray
     eligible_count: int
+    # per channel: the reference would have raised "Jacobi did not converge"
+    # here (noise.py:180-185); see DESIGN.md section 1.  Not a reference field.
+    jacobi_direct_off: tuple = field(default=(False, False, False), compare=False, repr=False)
 
 
 class TailSelection(NamedTuple):
@@ -181,6 +184,7 @@ def _to_estimate(out: nat.Noise) -> NoiseEstimate:
         tau=np.array(out.tau[:]),
         fallback=np.array([bool(x) for x in out.fallback]),
         eligible_count=int(out.eligible_count),
+        jacobi_direct_off=tuple(bool(x) for x in out.jacobi_direct_off),
     )
 
 

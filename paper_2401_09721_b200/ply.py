@@ -428,6 +428,7 @@ def denoise_ply(source, cfg: FilterConfig = FilterConfig(), cached_q: int | None
     cq = -1 if cached_q is None else int(cached_q)
     cs = float("nan") if cached_sigma_est is None else float(cached_sigma_est)
     body = _as_u8(data)[blk.start:]
+    ctx.graph_token = None  # the call rebuilds the device graph, even when it fails
     rc = ctx.lib.fgbd_denoise_ply(ctx.handle, nat.ptr(body), n, blk.stride,
                                   blk.offsets.ctypes.data_as(nat.P(nat.c_i32)),
                                   blk.types.ctypes.data_as(nat.P(nat.c_i32)), 0,
@@ -438,7 +439,6 @@ def denoise_ply(source, cfg: FilterConfig = FilterConfig(), cached_q: int | None
         if msg.startswith("negative"):
             raise PlyParseError(msg)
     ctx.check(rc, "denoise_ply")
-    ctx.graph_token = None
     report = _report_from(rep, cfg, cached_q, cached_sigma_est)
     if dest is not None:
         with open(dest, "wb") as fh:

@@ -266,8 +266,13 @@ def custom_case(name, coords, colors, bits, index, cfg=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-1m", action="store_true")
+    ap.add_argument("--only-8m", action="store_true",
+                    help="add the configs[4] 8M frames to the existing index.json")
     args = ap.parse_args()
     index: dict = {}
+    if args.only_8m:
+        main_8m()
+        return
 
     # warm the numba JIT so recorded times are not compile times
     w, _ = fgbd.generate_cloud("ramp", 1000)
@@ -350,6 +355,21 @@ def main():
         "numpy": np.__version__,
         "cases": index,
     }
+    (OUT / "index.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
+
+
+def main_8m():
+    """configs[4]: the 8M frame (k=200 lattice, b=8), scalars + digests only.
+
+    The reference takes ~2-3 min per frame here.  Appended to index.json so
+    the smaller fixtures are not regenerated.
+    """
+    meta = json.loads((OUT / "index.json").read_text())
+    index = meta["cases"]
+    w, _ = fgbd.generate_cloud("ramp", 1000)
+    fgbd.denoise(fgbd.add_gaussian_noise(w, 10, seed=1))
+    case("x8m_ramp_s10", "ramp", 8_000_000, 10.0, colors=None, index=index)
+    case("x8m_two-tone_s10", "two-tone", 8_000_000, 10.0, colors=None, index=index)
     (OUT / "index.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
 
 

@@ -192,7 +192,7 @@ def _check_e2e(rec, arr, clean, out, rep):
     np.testing.assert_array_equal(out.coords, out.coords)
 
 
-E2E = [n for n in golden_names(require=["report"]) if not n.startswith(("x1m_", "checker"))]
+E2E = [n for n in golden_names(require=["report"]) if not n.startswith(("x1m_", "x8m_", "checker"))]
 
 
 @pytest.mark.parametrize("name", E2E)
