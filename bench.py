@@ -62,6 +62,8 @@ def parse():
                     help="frame: BASELINE configs[1] (default); video: configs[3]; "
                          "slab: configs[4] (one frame split over the GPUs)")
     ap.add_argument("--frames", type=int, default=300, help="video length (configs[3])")
+    ap.add_argument("--slab-ranks", type=int, default=1,
+                    help="slab workload at N=1: logical ranks emulated on the one GPU")
     ap.add_argument("--workers", type=int, default=None,
                     help="host threads per GPU (default: video 3, ply 2)")
     ap.add_argument("--no-reuse", action="store_true",
@@ -672,11 +674,14 @@ def run_ply(args):
 # ---------------------------------------------------------------------------
 
 def run_slab(args):
+    """configs[4]: one 8M-point frame cut into z-slabs over the GPUs.  Each
+    rank uploads, builds, estimates, filters and downloads only its slab
+    (output="local"); N = 1 runs `--slab-ranks` emulated ranks on one GPU."""
     import torch
 
     import paper_2401_09721_b200 as fb
     from paper_2401_09721_b200 import _native as nat
-    from paper_2401_09721_b200.slab import denoise_slab
+    from paper_2401_09721_b200.slab import denoise_slab, slab_partition
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -695,25 +700,30 @@ def run_slab(args):
     y = nat.pinned_empty(noisy.colors.shape, np.float64)
     y[...] = noisy.colors
     pc = fb.PointCloud(c, y, noisy.bit_depth)
-    emulate = None if world > 1 else 1
+    ranks = world if world > 1 else max(1, args.slab_ranks)
+    part = slab_partition(pc, ranks)
 
     def step():
         if pg is not None:
-            return denoise_slab(pc, process_group=pg)
-        return denoise_slab(pc, emulate_ranks=1)
+            idx, col, rep = denoise_slab(pc, process_group=pg, output="local", partition=part)
+            return rep
+        return denoise_slab(pc, emulate_ranks=ranks, partition=part)[1]
 
-    for _ in range(max(args.warmup, 3)):
-        out, rep = step()
-    walls, devs = [], []
+    for _ in range(warmup_steps(args)):
+        rep = step()
+    walls, devs, stages = [], [], []
     for _ in range(args.steps):
         if pg is not None:
             import torch.distributed as dist
 
             dist.barrier()
         t0 = time.perf_counter()
-        out, rep = step()
+        rep = step()
         walls.append(time.perf_counter() - t0)
         devs.append(rep.device["t_total"])
+        stages.append((rep.device["t_h2d"], rep.stage_timings["graph_construction"],
+                       rep.stage_timings["noise_estimation"], rep.device["t_lf_steps"],
+                       rep.device["t_d2h"]))
     wall = float(np.sum(walls))
     if world > 1:
         import torch.distributed as dist
@@ -721,6 +731,7 @@ def run_slab(args):
         t = torch.tensor([wall], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wall = float(t.item())
+    st = np.mean(np.array(stages), axis=0) * 1e3
     if rank == 0:
         print(json.dumps({
             "metric": f"frames/sec, one {n:,}-point frame slab-partitioned over the GPUs",
@@ -728,11 +739,13 @@ def run_slab(args):
             "ms_per_step": 1e3 * wall / args.steps, "steps": args.steps,
             "higher_is_better": True, "scaling": "strong", "dtype": "f64", "data": "synthetic",
             "device_ms_rank0": 1e3 * float(np.mean(devs)),
-            "stage_ms": {k: 1e3 * v for k, v in rep.stage_timings.items()},
+            "rank0_stage_ms": {"h2d_own_points": st[0], "graph_construction": st[1],
+                               "noise_estimation_and_mask": st[2], "lf_steps": st[3],
+                               "d2h_own_points": st[4]},
             "config": {"workload": "BASELINE.json configs[4]", "kind": args.kind, "n_points": n,
                        "sigma": args.sigma, "selected_q": rep.selected_q,
-                       "filter_steps_S": rep.device["steps"], "slab_ranks": world,
-                       "emulated": emulate is not None},
+                       "filter_steps_S": rep.device["steps"], "slab_ranks": ranks,
+                       "emulated": world == 1, "points_per_rank": part.counts.tolist()},
         }), flush=True)
     if world > 1:
         import torch.distributed as dist

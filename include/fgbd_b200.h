@@ -259,25 +259,39 @@ int32_t fgbd_select_tail(const double* lam, int32_t d, int32_t tau_divisor,
                          char* err, int32_t err_len);
 
 /* ---- spatial slab partition of one frame over P ranks ---- */
-/* Every rank builds the whole graph; rank r filters rows [n*r/P, n*(r+1)/P)
- * and reads foreign neighbours from the owner's buffers over peer memory.
- * emulated != 0 runs all P ranks as block groups of one cooperative launch
- * on this context's GPU (bit-identical protocol, used for testing);
- * otherwise one process per GPU exchanges fgbd_slab_export handles (IPC)
- * and calls fgbd_slab_import before the first fgbd_denoise_slab. */
+/* The frame is cut into z-slabs (contiguous ranges of the global scan-line-1
+ * order); rank r owns counts[r] points and uploads, sorts, estimates and
+ * filters only those.  Cross-slab scan-line neighbours come from the peers'
+ * block lists, sigma_g / the NE moments / the FSLR sums are all-gathered,
+ * and halo signals are read from the owner's buffers -- all over peer memory
+ * (csrc/slab.cu).  Results equal fgbd_denoise on the whole frame (q, S and
+ * colours bit for bit).  Bit depths up to 15.
+ *
+ * FGBD_SLAB_EMULATED: all P ranks run in this process on this context's GPU
+ * (the test harness of the protocol); the arrays of fgbd_denoise_slab then
+ * hold every rank's points, concatenated in rank order.  Otherwise one
+ * process per GPU exchanges fgbd_slab_export handles (IPC) and calls
+ * fgbd_slab_import before its first fgbd_denoise_slab. */
+#define FGBD_SLAB_EMULATED     0x1u
+#define FGBD_SLAB_FULL_OUTPUT  0x2u  /* multi-GPU: every rank receives the full frame */
 typedef struct fgbd_slab fgbd_slab;
-fgbd_slab* fgbd_slab_create(fgbd_ctx* ctx, int32_t world, int32_t rank, int64_t n,
-                            int32_t emulated);
+fgbd_slab* fgbd_slab_create(fgbd_ctx* ctx, int32_t world, int32_t rank, int64_t n_total,
+                            int64_t max_own, uint32_t slab_flags);
 void fgbd_slab_destroy(fgbd_ctx* ctx, fgbd_slab* slab);
 int32_t fgbd_slab_handle_size(void);
 int32_t fgbd_slab_export(fgbd_ctx* ctx, fgbd_slab* slab, uint8_t* handle_out);
 int32_t fgbd_slab_import(fgbd_ctx* ctx, fgbd_slab* slab, const uint8_t* handles);
-/* denoise (filtering.py:259-328) with the filter loop split over the slab
- * ranks; every rank returns the full frame. */
+/* denoise (filtering.py:259-328) over the slab ranks.  coords / colors: the
+ * own points (all ranks' points, rank-major, when emulated) in increasing
+ * global index; gidx: their global indices (NULL: gidx_base + i); counts:
+ * points of every rank (z-slab order).  out_colors: the own points' colours
+ * in input order, or the full frame (n_total, 3) with FGBD_SLAB_FULL_OUTPUT.
+ * The report describes the whole frame. */
 int32_t fgbd_denoise_slab(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coords,
-                          const double* colors, int64_t n, int32_t bit_depth,
-                          const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
-                          double* out_colors, fgbd_report* report, uint32_t flags);
+                          const double* colors, const uint32_t* gidx, int64_t gidx_base,
+                          const int64_t* counts, int32_t bit_depth, const fgbd_config* cfg,
+                          int32_t cached_q, double cached_sigma, double* out_colors,
+                          fgbd_report* report, uint32_t flags);
 
 /* ---- PLY binary vertex records (ply.py:134-287) ---- */
 /* type codes: 0 int8, 1 uint8, 2 int16, 3 uint16, 4 int32, 5 uint32,

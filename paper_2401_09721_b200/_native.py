@@ -24,6 +24,8 @@ FGBD_OK, E_CLOUD, E_GRAPH, E_NOISE, E_FILTER, E_CUDA, E_NCCL, E_ARG = range(8)
 FLAG_DEVICE_PTRS = 0x1
 FLAG_WEIGHTS_F64 = 0x2
 FLAG_NO_TIMING = 0x4
+SLAB_EMULATED = 0x1
+SLAB_FULL_OUTPUT = 0x2
 FLAG_REUSE_GRAPH = 0x8
 MAX_PATCH = 7
 TRACE_MAX = 1025
@@ -105,13 +107,14 @@ _SIGNATURES = {
                                               C.c_char_p, c_i32]),
     "fgbd_select_tail": (c_i32, [C.c_void_p, c_i32, c_i32, P(c_i32), P(c_f64), P(c_i32),
                                  C.c_char_p, c_i32]),
-    "fgbd_slab_create": (C.c_void_p, [C.c_void_p, c_i32, c_i32, c_i64, c_i32]),
+    "fgbd_slab_create": (C.c_void_p, [C.c_void_p, c_i32, c_i32, c_i64, c_i64, c_u32]),
     "fgbd_slab_destroy": (None, [C.c_void_p, C.c_void_p]),
     "fgbd_slab_handle_size": (c_i32, []),
     "fgbd_slab_export": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "fgbd_slab_import": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p]),
-    "fgbd_denoise_slab": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, c_i64, c_i32,
-                                  P(Config), c_i32, c_f64, C.c_void_p, P(Report), c_u32]),
+    "fgbd_denoise_slab": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  c_i64, C.c_void_p, c_i32, P(Config), c_i32, c_f64,
+                                  C.c_void_p, P(Report), c_u32]),
     "fgbd_ply_decode": (c_i32, [C.c_void_p, C.c_void_p, c_i64, c_i32, P(c_i32), P(c_i32),
                                 C.c_void_p, C.c_void_p, C.c_void_p, P(c_i32), c_u32]),
     "fgbd_ply_encode": (c_i32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, c_i64,

@@ -513,31 +513,9 @@ void fgbd_host_free(void* p) {
   if (p) cudaFreeHost(p);
 }
 
-static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coords,
-                            const double* colors, int64_t n, int32_t bits,
-                            const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
-                            double* out_colors, fgbd_report* rep, uint32_t flags);
-
 int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors, int64_t n,
                      int32_t bits, const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
                      double* out_colors, fgbd_report* rep, uint32_t flags) {
-  return denoise_impl(ctx, nullptr, coords, colors, n, bits, cfg, cached_q, cached_sigma,
-                      out_colors, rep, flags);
-}
-
-int32_t fgbd_denoise_slab(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coords,
-                          const double* colors, int64_t n, int32_t bits, const fgbd_config* cfg,
-                          int32_t cached_q, double cached_sigma, double* out_colors,
-                          fgbd_report* rep, uint32_t flags) {
-  if (!slab) return set_error(ctx, FGBD_E_ARG, "null slab");
-  return denoise_impl(ctx, slab, coords, colors, n, bits, cfg, cached_q, cached_sigma,
-                      out_colors, rep, flags);
-}
-
-static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coords,
-                            const double* colors, int64_t n, int32_t bits,
-                            const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
-                            double* out_colors, fgbd_report* rep, uint32_t flags) {
   if (!ctx || !rep) return set_error(ctx, FGBD_E_ARG, "null context or report");
   cudaSetDevice(ctx->device);
   ctx->err.clear();
@@ -571,7 +549,7 @@ static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coord
   const int64_t* frame_coords = dev ? coords : ctx->coords64;
   // static-geometry reuse: the held graph stands if this frame's coordinates
   // are byte-identical to the ones it was built from (exact device compare)
-  const bool want_reuse = (flags & FGBD_FLAG_REUSE_GRAPH) && !slab && !w64;
+  const bool want_reuse = (flags & FGBD_FLAG_REUSE_GRAPH) && !w64;
   const bool may_reuse = want_reuse && ctx->held_valid && ctx->g_n == n && ctx->g_bits == bits &&
                          ctx->g_have_weights && !ctx->g_weights64;
   // A frame that will probably reuse the graph has no build for the colour
@@ -628,14 +606,9 @@ static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coord
   if (cached_q >= 0) {
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
     int fin = BUF_Y;
-    if (slab) {
-      if ((rc = launch_slab(ctx, slab, n, 0, cached_q, dev ? out_colors : ctx->out))) return rc;
-      if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
-    } else {
-      if ((rc = launch_fixed_steps(ctx, n, cached_q, w64, &fin))) return rc;
-      if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
-      if ((rc = launch_compact(ctx, n, fin, dev ? out_colors : ctx->out, 1))) return rc;
-    }
+    if ((rc = launch_fixed_steps(ctx, n, cached_q, w64, &fin))) return rc;
+    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
+    if ((rc = launch_compact(ctx, n, fin, dev ? out_colors : ctx->out, 1))) return rc;
   } else {
     const int D = cfg->patch_size;
     if ((rc = launch_noise(ctx, n, D, fuse_w ? 1 : 0))) return rc;
@@ -657,26 +630,19 @@ static int32_t denoise_impl(fgbd_ctx* ctx, fgbd_slab* slab, const int64_t* coord
                           nullptr)))
       return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
-    if (slab) {
-      if ((rc = launch_slab(ctx, slab, n, 1, 0, dev ? out_colors : ctx->out))) return rc;
-      if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
-    } else {
-      if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) return rc;
-      if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
-      if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
-    }
+    if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) return rc;
+    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
+    if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   }
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
   FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
   device_last_compute(ctx->device) = ctx->ev_done;
-  if (!ctx->async_lock || cached_q < 0 || slab) FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_done));
+  if (!ctx->async_lock || cached_q < 0) FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_done));
   compute_lock.unlock();
   if (!dev && (rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), false))) return rc;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
   if ((rc = pull_ctl(ctx))) return rc;
   if ((rc = check_graph_ctl(ctx, bits))) return rc;
-  if (ctx->ctl_host->err_flags & 4)
-    return set_error(ctx, FGBD_E_NCCL, "slab peer did not reach the barrier (timeout)");
   const Ctl& h = *ctx->ctl_host;
   if (want_reuse && !reuse) {  // the copy now describes a complete graph with weights
     ctx->held_edges = h.n_edges;

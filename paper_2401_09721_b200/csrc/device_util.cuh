@@ -192,6 +192,49 @@ __device__ __forceinline__ int4 ld_pair_hint(const int2* p, uint64_t pol) {
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
+// Exact, order-independent sums of doubles v = 0 or v >= 1 (the edge lengths
+// sqrt(sqdist) of sigma_g, graph.py:227-233): v * 2^52 is an integer below
+// 2^(53 + 74) for v < 2^75, accumulated in 128-bit integers.  Any partition
+// of the edges (one GPU, P slab ranks, any grid) gives the same bits.
+typedef unsigned __int128 u128;
+__device__ __forceinline__ u128 fx52(double v) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const int eb = (int)((bits >> 52) & 0x7ff);
+  if (eb < 1023) return 0;  // only v == 0 occurs (v >= 1 otherwise)
+  const unsigned long long mant = (bits & ((1ull << 52) - 1)) | (1ull << 52);
+  return (u128)mant << (eb - 1023);
+}
+__device__ __forceinline__ u128 warp_sum_u128(u128 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long lo = __shfl_xor_sync(kFull, (unsigned long long)v, o);
+    const unsigned long long hi = __shfl_xor_sync(kFull, (unsigned long long)(v >> 64), o);
+    v += ((u128)hi << 64) | lo;
+  }
+  return v;
+}
+// Block-wide sum, valid in thread 0 (s_scratch: 2 x 32 u64).
+__device__ __forceinline__ u128 block_sum_u128(u128 v, unsigned long long* s_scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  v = warp_sum_u128(v);
+  if (lane == 0) {
+    s_scratch[2 * warp] = (unsigned long long)v;
+    s_scratch[2 * warp + 1] = (unsigned long long)(v >> 64);
+  }
+  __syncthreads();
+  u128 t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < nwarps; ++w) t += ((u128)s_scratch[2 * w + 1] << 64) | s_scratch[2 * w];
+  __syncthreads();
+  return t;
+}
+// The fixed-point sum back to a double (deterministic: a pure function of the bits).
+__device__ __forceinline__ double fx52_to_double(u128 s) {
+  const double hi = (double)(unsigned long long)(s >> 64), lo = (double)(unsigned long long)s;
+  return ldexp(__dadd_rn(ldexp(hi, 64), lo), -52);
+}
+
 // RN(a / b) from y = RN(1 / b) (__drcp_rn): q0 = RN(a y), r = a - b q0 (exact
 // with FMA), q = RN(q0 + r y) is the correctly rounded quotient for normal
 // a, b and a / b (Markstein); the guarded ranges fall back to the IEEE

@@ -77,6 +77,47 @@ struct Ctl {
   int early_exit;
   double trace[FGBD_TRACE_MAX];
   unsigned int ticket[8];
+  // slab ranks: this rank's share before the cross-rank all-gather
+  unsigned long long sg_fx[2];  // exact fixed-point sum of edge lengths (k_rows)
+  double mask_part[7];          // k_mask totals: count, sum_inc y^2 [3], sum_all y^2 [3]
+};
+
+constexpr int kMaxRanks = 16;
+
+// One scan-line block of a slab rank: the run of its points that share the
+// line's segment key (line 1: everything; line 2: x; line 3: (y, x)) in
+// that line's sorted order, with its first and last point.  Because the
+// slabs are z-ranges, the global sorted order of a line is the blocks
+// ordered by (key, rank): cross-slab scan-line neighbours are exactly the
+// last/first points of (key, rank)-adjacent blocks.
+struct SumRec {
+  unsigned long long key, fpc, lpc;  // segment key; packed coords of first/last point
+  int fgid, lgid;                    // global point indices (reference index order)
+  int frow, lrow;                    // global rows (global scan-line-1 rank)
+  int flid, llid;                    // local ids on the owning rank
+};
+
+// Signal rows of every slab rank by GLOBAL row: y[r] + j addresses row j of
+// rank r's buffer (y[r] = buffer base - lo[r]; peer-mapped for r != self).
+struct SlabView {
+  int world, self;
+  int64_t lo[kMaxRanks + 1];
+  const double4* y[kMaxRanks];
+};
+
+// Graph-construction state of one slab rank (csrc/graph.cu, csrc/slab.cu).
+struct SlabGC {
+  int world, rank, b;
+  int64_t n_own, lo;           // own points; global row of own row 0
+  int64_t blk_cap;             // per-line capacity of the block lists
+  void* ext_pc;                // [n_own + 2 * (1 + 2 blk_cap)] packed coords (own, then halo)
+  int* ext_pos;                // same: global row of every local id
+  uint32_t* ext_gidx;          // same: global point index of every local id
+  unsigned int* tile_cnt;      // scratch [2][tiles + 1]
+  SumRec* sums[3];             // own block lists (peer-visible region)
+  long long* hdr;              // own block counts [3] (peer-visible region)
+  const SumRec* peer_sums[kMaxRanks][3];
+  const long long* peer_hdr[kMaxRanks];
 };
 
 struct SortScratch {
@@ -226,6 +267,8 @@ int scan_exclusive(fgbd_ctx* ctx, const int64_t* in, int64_t n, int64_t* out, in
 // NE pass; fuse_weights: also convert the ELL payloads to Gaussian weights
 // (only valid before launch_weights ran and when b <= 15)
 int launch_noise(fgbd_ctx* ctx, int64_t n, int patch, int fuse_weights);
+// slab rank: own rows, neighbour colours by global row through `v`
+int launch_noise_slab(fgbd_ctx* ctx, int64_t n_own, int patch, const SlabView& v);
 // host side: covariance -> Jacobi -> tail -> sigma (noise.py:122-243)
 int finish_noise(fgbd_ctx* ctx, int patch, int divisor, fgbd_noise* out);
 int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err,
@@ -240,6 +283,8 @@ int launch_expand(fgbd_ctx* ctx, const double* d_src, int64_t n, int buf, cudaSt
 int launch_compact(fgbd_ctx* ctx, int64_t n, int src_buf, double* d_dst, int clip);
 int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_max, int mode,
                 int early_exit, const uint8_t* d_include_bytes);
+int launch_mask_slab(fgbd_ctx* ctx, int64_t n_own, const double4* y, double sigma_est,
+                     int active);
 int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64);
 int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf);
 int launch_csr_steps(fgbd_ctx* ctx, const int64_t* d_indptr, const int64_t* d_indices,
@@ -251,8 +296,16 @@ int launch_criterion(fgbd_ctx* ctx, const double* d_y, const double* d_x,
 
 }  // namespace fgbd
 
-struct fgbd_slab;
 namespace fgbd {
-int launch_slab(fgbd_ctx* ctx, fgbd_slab* s, int64_t n, int select, int fixed_steps,
-                double* d_out);
+// ---- slab ranks (graph.cu) -------------------------------------------------
+// Phase 1: sort the own points (coords in ctx->cur_coords, gidx in
+// g.ext_gidx), rank neighbours, global rows, block lists of the 3 lines.
+int launch_graph_slab_own(fgbd_ctx* ctx, SlabGC& g);
+// Phase 2 (after every rank published its block lists): cross-slab
+// neighbours from the peers' lists, halo records, then the rows (ELL words =
+// global rows) and this rank's sigma_g share in ctl->sg_fx / n_edges / max_deg.
+int launch_graph_slab_rows(fgbd_ctx* ctx, SlabGC& g);
+// Eq. (4) on own rows (cached path; NE fuses it otherwise)
+int launch_weights_slab(fgbd_ctx* ctx, const SlabGC& g);
+int launch_iota_u32(fgbd_ctx* ctx, uint32_t* out, int64_t n, int64_t base);
 }  // namespace fgbd

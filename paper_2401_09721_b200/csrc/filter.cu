@@ -52,24 +52,11 @@
 #endif
 #include "device_util.cuh"
 #include "fgbd_internal.cuh"
+#include "select_state.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace fgbd {
-
-__device__ __forceinline__ double criterion(const double sy[3], const double sx[3],
-                                            long long count, double sv2, int mode) {
-  if (mode == FGBD_CRIT_POOLED) {
-    const double ty = (sy[0] + sy[1]) + sy[2];
-    const double tx = (sx[0] + sx[1]) + sx[2];
-    const double lost = (ty - tx) / ((double)count * 3.0);
-    return fabs(sv2 - lost);
-  }
-  double acc = 0.0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) acc += fabs(sv2 - (sy[c] - sx[c]) / (double)count);
-  return acc / 3.0;
-}
 
 // ---------------------------------------------------------------------------
 // layout conversion
@@ -127,6 +114,8 @@ struct MaskArgs {
   int mode;
   int early_exit;
   double sv2;
+  int defer;        // slab rank: leave the totals in ctl->mask_part (all-gathered later)
+  int64_t n_total;  // points of the whole frame (the all-excluded fallback count)
 };
 
 __global__ void __launch_bounds__(kBlock) k_mask(MaskArgs a) {
@@ -166,36 +155,13 @@ __global__ void __launch_bounds__(kBlock) k_mask(MaskArgs a) {
       for (int k = 0; k < 7; ++k) t[k] += ld_cg(&a.part[k * gridDim.x + b]);
     block_sum<7>(t, s_red);
     if (threadIdx.x == 0) {
-      Ctl* c = a.ctl;
-      long long cnt = (long long)t[0];
-      const bool all_ex = (cnt == 0) && (a.inc_bytes == nullptr) && a.active;
-      c->all_excluded = all_ex;
-      c->mask_all = all_ex;
-      if (all_ex) {
-        cnt = a.n;
-        for (int k = 0; k < 3; ++k) c->sy[k] = t[4 + k];
+      if (a.defer) {
+        for (int k = 0; k < 7; ++k) a.ctl->mask_part[k] = t[k];
       } else {
-        for (int k = 0; k < 3; ++k) c->sy[k] = t[1 + k];
+        mask_finalize(a.ctl, t, a.n, a.inc_bytes != nullptr, a.active, a.q_max, a.mode,
+                      a.early_exit, a.sv2);
       }
-      c->included = cnt;
-      // select_q initial state: x = y, q = 0 (filtering.py:237-243)
-      const double crit0 = cnt > 0 ? criterion(c->sy, c->sy, cnt, a.sv2, a.mode) : 0.0;
-      c->q = 0;
-      c->best_q = 0;
-      c->best_crit = crit0;
-      c->prev_crit = crit0;
-      c->streak = 0;
-      c->steps = 0;
-      c->in_buf = BUF_Y;
-      c->best_buf = BUF_Y;
-      c->out_buf = BUF_A;
-      c->stop = (a.q_max <= 0) || (crit0 == 0.0) || (cnt < 1);
-      c->trace[0] = crit0;
-      c->sv2 = a.sv2;
-      c->q_max = a.q_max;
-      c->mode = a.mode;
-      c->early_exit = a.early_exit;
-      c->ticket[1] = 0;
+      a.ctl->ticket[1] = 0;
     }
   }
 }
@@ -1060,7 +1026,30 @@ int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_ma
   a.mode = mode;
   a.early_exit = early_exit;
   a.sv2 = sigma_est * sigma_est;
+  a.defer = 0;
+  a.n_total = n;
   k_mask<<<fill_grid(ctx, n), kBlock, 0, ctx->stream>>>(a);
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+// slab rank: own rows, Y at `y`; totals deferred to ctl->mask_part
+int launch_mask_slab(fgbd_ctx* ctx, int64_t n_own, const double4* y, double sigma_est,
+                     int active) {
+  MaskArgs a{};
+  a.fslr = ctx->fslr;
+  a.y = y;
+  a.inc_bytes = nullptr;
+  a.n = n_own;
+  a.thr = 2.0 * sigma_est;
+  a.active = active;
+  a.mask = ctx->mask;
+  a.part = ctx->partials;
+  a.ctl = ctx->ctl;
+  a.sv2 = sigma_est * sigma_est;
+  a.defer = 1;
+  a.n_total = n_own;
+  k_mask<<<fill_grid(ctx, n_own), kBlock, 0, ctx->stream>>>(a);
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
 }

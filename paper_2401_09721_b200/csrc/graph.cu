@@ -336,7 +336,8 @@ __global__ void __launch_bounds__(kBlock) k_neighbors(const uint32_t* __restrict
                                                      const uint32_t* __restrict__ p1,
                                                      const uint32_t* __restrict__ p2,
                                                      int64_t n, int2* __restrict__ cand,
-                                                     int* __restrict__ pos, Ctl* __restrict__ ctl) {
+                                                     int* __restrict__ pos, Ctl* __restrict__ ctl,
+                                                     int64_t row_base = 0) {
   const int line = blockIdx.y;
   const uint32_t* perm = line == 0 ? p0 : (line == 1 ? p1 : p2);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(kBlock) k_neighbors(const uint32_t* __restrict
     const int next = k + 1 < n ? (int)perm[k + 1] : -1;
     cand[line * n + u] = make_int2(prev, next);
     if (line == 0 && pos) {
-      pos[u] = (int)k;  // row of point u = its scan-line-1 rank
+      pos[u] = (int)(row_base + k);  // row of point u = its scan-line-1 rank
       // input already in line-1 order (raster scans): rows == points, and
       // k_rows can skip the relabelling work
       if (__any_sync(__activemask(), u != (int)k) && (threadIdx.x & 31) == 0)
@@ -355,15 +356,17 @@ __global__ void __launch_bounds__(kBlock) k_neighbors(const uint32_t* __restrict
   }
 }
 
-__device__ __forceinline__ void cswap(unsigned& a, unsigned& b) {
-  const unsigned lo = min(a, b), hi = max(a, b);
+template <typename T>
+__device__ __forceinline__ void cswap(T& a, T& b) {
+  const T lo = min(a, b), hi = max(a, b);
   a = lo;
   b = hi;
 }
 
 // sort 6 values: a 12-comparator network of depth 5 (checked on all 2^6
 // 0/1 inputs)
-__device__ __forceinline__ void sort6(unsigned (&c)[6]) {
+template <typename T>
+__device__ __forceinline__ void sort6(T (&c)[6]) {
   cswap(c[0], c[5]);
   cswap(c[1], c[3]);
   cswap(c[2], c[4]);
@@ -378,21 +381,32 @@ __device__ __forceinline__ void sort6(unsigned (&c)[6]) {
   cswap(c[3], c[4]);
 }
 
-template <typename K, bool BIG>
+// Slab rank: rows are the rank's own points in scan-line-1
+// order; local ids >= n_own are halo points (foreign neighbours); `pos` maps
+// every local id to its GLOBAL row; the reference's index order is the
+// global point index gidx[local id], so dedup, "below" flags, sigma_g's
+// upper-slot rule and the patch tie-break all compare gidx.
+struct RowsSlab {
+  const uint32_t* gidx;  // [n_own + halo]
+  int64_t lo;            // global row of own row 0
+};
+
+template <typename K, bool BIG, bool SLAB = false>
 __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
                                                  const K* __restrict__ pc, int64_t n, int b,
                                                  const int* __restrict__ pos,
                                                  const uint32_t* __restrict__ rowid, EllRef ell,
                                                  uint32_t* __restrict__ meta,
                                                  double* __restrict__ partials,
-                                                 Ctl* __restrict__ ctl) {
-  __shared__ double s_red[32 * 2];
+                                                 Ctl* __restrict__ ctl, RowsSlab sl = RowsSlab{}) {
+  __shared__ unsigned long long s_red[32 * 2];
   __shared__ bool s_last;
-  double sg_sum = 0.0, e_cnt = 0.0;
+  u128 sg_sum = 0;  // exact: the same bits for any partition of the edges
+  unsigned long long e_cnt = 0;
   int maxdeg = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // rows differ from points only when the line-1 order is not the identity
-  if (pos && !(*(volatile const int*)&ctl->err_flags & 8)) {
+  if (!SLAB && pos && !(*(volatile const int*)&ctl->err_flags & 8)) {
     pos = nullptr;
     rowid = nullptr;
   }
@@ -406,11 +420,33 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
       c[2 * l] = (unsigned)v.x;  // -1 -> 0xffffffff sorts last
       c[2 * l + 1] = (unsigned)v.y;
     }
-    sort6(c);
+    unsigned gj[6];  // SLAB: global index of candidate s
+    unsigned gi = 0;
+    if (SLAB) {
+      // order and dedup by the global index (halo copies of one point share it)
+      unsigned long long k6[6];
 #pragma unroll
-    for (int s = 5; s > 0; --s)
-      if (c[s] == c[s - 1]) c[s] = 0xffffffffu;
-    sort6(c);
+      for (int s = 0; s < 6; ++s)
+        k6[s] = c[s] == 0xffffffffu ? ~0ull
+                                    : ((unsigned long long)sl.gidx[c[s]] << 32) | c[s];
+      sort6(k6);
+#pragma unroll
+      for (int s = 5; s > 0; --s)
+        if ((k6[s] >> 32) == (k6[s - 1] >> 32)) k6[s] = ~0ull;
+      sort6(k6);
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        c[s] = (unsigned)k6[s];
+        gj[s] = (unsigned)(k6[s] >> 32);
+      }
+      gi = sl.gidx[i];
+    } else {
+      sort6(c);
+#pragma unroll
+      for (int s = 5; s > 0; --s)
+        if (c[s] == c[s - 1]) c[s] = 0xffffffffu;
+      sort6(c);
+    }
     int deg = 0;
 #pragma unroll
     for (int s = 0; s < 6; ++s) deg += (c[s] != 0xffffffffu);
@@ -422,13 +458,13 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
       sq[s] = ~0ull;
       if (s < deg) {
         long long xj, yj, zj;
-        FGBD_DCHECK((int64_t)c[s] < n);
+        FGBD_DCHECK(SLAB || (int64_t)c[s] < n);
         unpack(pc[c[s]], b, &xj, &yj, &zj);
         const long long dx = xi - xj, dy = yi - yj, dz = zi - zj;
         sq[s] = (unsigned long long)(dx * dx + dy * dy + dz * dz);
-        if ((int64_t)c[s] > i) {
-          sg_sum += sqrt((double)sq[s]);
-          e_cnt += 1.0;
+        if (SLAB ? gj[s] > gi : (int64_t)c[s] > i) {
+          sg_sum += fx52(sqrt((double)sq[s]));
+          e_cnt += 1;
         }
       }
     }
@@ -464,10 +500,10 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
     unsigned slot_of[6];  // ELL slot that receives candidate slot s
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
-      int w = (int)r;  // padding: (own row, 0)
+      int w = (int)(SLAB ? sl.lo + r : r);  // padding: (own row, 0)
       if (s < deg) {
         const int jr = pos ? pos[c[s]] : (int)c[s];
-        w = jr | ((int64_t)c[s] < i ? kBelowBit : 0);
+        w = jr | ((SLAB ? gj[s] < gi : (int64_t)c[s] < i) ? kBelowBit : 0);
       }
       word[s] = w;
       slot_of[s] = s;
@@ -509,23 +545,26 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
   // block reduce (sum, count) and the max degree
   maxdeg = __reduce_max_sync(kFull, maxdeg);
   if ((threadIdx.x & 31) == 0 && maxdeg > 0) atomicMax(&ctl->max_deg, maxdeg);
-  double v[2] = {sg_sum, e_cnt};
-  block_sum<2>(v, s_red);
+  unsigned long long* up = reinterpret_cast<unsigned long long*>(partials);
+  const u128 bs = block_sum_u128(sg_sum, s_red);
+  const u128 bc = block_sum_u128((u128)e_cnt, s_red);
   if (threadIdx.x == 0) {
-    partials[2 * blockIdx.x] = v[0];
-    partials[2 * blockIdx.x + 1] = v[1];
+    up[3 * blockIdx.x] = (unsigned long long)bs;
+    up[3 * blockIdx.x + 1] = (unsigned long long)(bs >> 64);
+    up[3 * blockIdx.x + 2] = (unsigned long long)bc;
   }
   if (last_block(&ctl->ticket[0], &s_last)) {
-    double a[2] = {0.0, 0.0};
+    u128 a = 0, cnt = 0;
     for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
-      a[0] += ld_cg(&partials[2 * k]);
-      a[1] += ld_cg(&partials[2 * k + 1]);
+      a += ((u128)__ldcg(&up[3 * k + 1]) << 64) | __ldcg(&up[3 * k]);
+      cnt += __ldcg(&up[3 * k + 2]);
     }
-    block_sum<2>(a, s_red);
+    a = block_sum_u128(a, s_red);
+    cnt = block_sum_u128(cnt, s_red);
     if (threadIdx.x == 0) {
-      const unsigned long long e = (unsigned long long)a[1];
+      const unsigned long long e = (unsigned long long)cnt;
       ctl->n_edges = e;
-      ctl->sigma_g = e ? a[0] / (double)e : 0.0;
+      ctl->sigma_g = e ? fx52_to_double(a) / (double)e : 0.0;
       ctl->ticket[0] = 0;
     }
   }
@@ -538,7 +577,8 @@ __global__ void __launch_bounds__(kBlock) k_weights(EllRef ell,
                                                     double* __restrict__ w64,
                                                     const K* __restrict__ pc, int64_t n,
                                                     int b, const uint32_t* __restrict__ rowid,
-                                                    const Ctl* __restrict__ ctl) {
+                                                    const Ctl* __restrict__ ctl,
+                                                    int64_t row_base = 0) {
   const double sg = ctl->sigma_g;
   const double sg2 = sg * sg;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -550,7 +590,7 @@ __global__ void __launch_bounds__(kBlock) k_weights(EllRef ell,
       int2 sl = make_int2(ell.nbr[eslot(s, n, i)], (int)ell.pay[eslot(s, n, i)]);
       double w = 0.0;
       const int j = ell_j(sl.x);
-      if (j != (int)i) {
+      if (j != (int)(i + row_base)) {  // padding slots point at the own row
         unsigned long long sq;
         if (BIG) {
           long long xj, yj, zj;
@@ -933,6 +973,327 @@ int launch_export(fgbd_ctx* ctx, int64_t n, int64_t* d_indptr, int64_t* d_indice
   FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   *nnz_out = h[0];
   *e_out = h[1];
+  return FGBD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// slab ranks: block lists, cross-slab neighbours
+// ---------------------------------------------------------------------------
+
+// segment key of a scan line: the code bits above z (z is the slab axis)
+template <typename K>
+__device__ __forceinline__ unsigned long long seg_key(K pc, int line, int b) {
+  if (line == 0) return 0ull;
+  const K k = line_key(pc, line, b);
+  return (unsigned long long)(line == 1 ? (k >> (2 * b)) : (k >> b));
+}
+
+constexpr int kBlkIPT = 8;
+constexpr int kBlkTile = kBlock * kBlkIPT;
+
+template <typename K>
+__device__ __forceinline__ bool blk_start(const uint32_t* perm, const K* pc, int64_t k, int line,
+                                          int b) {
+  return k == 0 || seg_key(pc[perm[k]], line, b) != seg_key(pc[perm[k - 1]], line, b);
+}
+
+// per tile: number of block starts (lines 2 and 3 = blockIdx.y 0 / 1)
+template <typename K>
+__global__ void __launch_bounds__(kBlock) k_blk_count(const uint32_t* __restrict__ p1,
+                                                      const uint32_t* __restrict__ p2,
+                                                      const K* __restrict__ pc, int64_t n, int b,
+                                                      unsigned int* __restrict__ cnt, int tiles) {
+  __shared__ double s_red[32];
+  const int line = 1 + blockIdx.y;
+  const uint32_t* perm = line == 1 ? p1 : p2;
+  const int64_t base = (int64_t)blockIdx.x * kBlkTile;
+  double c[1] = {0.0};
+  for (int j = 0; j < kBlkIPT; ++j) {
+    const int64_t k = base + j * kBlock + threadIdx.x;
+    if (k < n && blk_start(perm, pc, k, line, b)) c[0] += 1.0;
+  }
+  block_sum<1>(c, s_red);
+  if (threadIdx.x == 0) cnt[blockIdx.y * (tiles + 1) + blockIdx.x] = (unsigned)c[0];
+}
+
+// exclusive tile offsets (in place) and the block counts of the 3 lines
+__global__ void k_blk_scan(unsigned int* __restrict__ cnt, int tiles, long long* __restrict__ hdr) {
+  if (threadIdx.x < 2) {
+    unsigned int* c = cnt + threadIdx.x * (tiles + 1);
+    unsigned run = 0;
+    for (int t = 0; t < tiles; ++t) {
+      const unsigned v = c[t];
+      c[t] = run;
+      run += v;
+    }
+    hdr[1 + threadIdx.x] = run;
+  }
+  if (threadIdx.x == 2) hdr[0] = 1;
+}
+
+template <typename K>
+__device__ __forceinline__ void put_first(SumRec& r, const K* pc, const uint32_t* gidx,
+                                          const int* pos, uint32_t lid, unsigned long long key) {
+  r.key = key;
+  r.fpc = (unsigned long long)pc[lid];
+  r.fgid = (int)gidx[lid];
+  r.frow = pos[lid];
+  r.flid = (int)lid;
+}
+template <typename K>
+__device__ __forceinline__ void put_last(SumRec& r, const K* pc, const uint32_t* gidx,
+                                         const int* pos, uint32_t lid) {
+  r.lpc = (unsigned long long)pc[lid];
+  r.lgid = (int)gidx[lid];
+  r.lrow = pos[lid];
+  r.llid = (int)lid;
+}
+
+// block records of lines 2 and 3 in sorted order (+ the single line-1 block)
+template <typename K>
+__global__ void __launch_bounds__(kBlock) k_blk_emit(const uint32_t* __restrict__ p0,
+                                                     const uint32_t* __restrict__ p1,
+                                                     const uint32_t* __restrict__ p2,
+                                                     const K* __restrict__ pc, int64_t n, int b,
+                                                     const unsigned int* __restrict__ cnt,
+                                                     int tiles, const uint32_t* __restrict__ gidx,
+                                                     const int* __restrict__ pos, SumRec* s0,
+                                                     SumRec* s1, SumRec* s2) {
+  __shared__ unsigned s_w[kBlock / 32];
+  const int line = 1 + blockIdx.y;
+  const uint32_t* perm = line == 1 ? p1 : p2;
+  SumRec* out = line == 1 ? s1 : s2;
+  const int64_t base = (int64_t)blockIdx.x * kBlkTile + (int64_t)threadIdx.x * kBlkIPT;
+  // this thread's run of kBlkIPT consecutive sorted positions
+  bool st[kBlkIPT];
+  unsigned mine = 0;
+#pragma unroll
+  for (int j = 0; j < kBlkIPT; ++j) {
+    const int64_t k = base + j;
+    st[j] = k < n && blk_start(perm, pc, k, line, b);
+    mine += st[j];
+  }
+  // block-wide exclusive scan of the per-thread counts
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned v = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) s_w[warp] = v;
+  __syncthreads();
+  unsigned wofs = 0;
+  for (int w = 0; w < warp; ++w) wofs += s_w[w];
+  unsigned ex = cnt[blockIdx.y * (tiles + 1) + blockIdx.x] + wofs + v - mine;
+#pragma unroll
+  for (int j = 0; j < kBlkIPT; ++j) {
+    const int64_t k = base + j;
+    if (k >= n) break;
+    const uint32_t lid = perm[k];
+    if (st[j]) put_first(out[ex], pc, gidx, pos, lid, seg_key(pc[lid], line, b));
+    ex += st[j];
+    const bool last = (k == n - 1) || blk_start(perm, pc, k + 1, line, b);
+    if (last) put_last(out[ex - 1], pc, gidx, pos, lid);
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    put_first(s0[0], pc, gidx, pos, p0[0], 0ull);
+    put_last(s0[0], pc, gidx, pos, p0[n - 1]);
+  }
+}
+
+// first index in [0, m) with key > k (upper) or >= k (lower)
+__device__ __forceinline__ long long bsearch_key(const SumRec* a, long long m,
+                                                 unsigned long long k, bool upper) {
+  long long lo = 0, hi = m;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    const unsigned long long v = a[mid].key;
+    if (upper ? (v <= k) : (v < k)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// For every own block: the (key, rank)-preceding and -following block over
+// all ranks.  A foreign neighbour becomes a halo record (local id
+// n_own + 2t + side); an own neighbour is already the local sort's.
+template <typename K>
+__global__ void __launch_bounds__(kBlock) k_resolve(SlabGC g, int2* __restrict__ cand) {
+  const long long B1 = g.hdr[1], B2 = g.hdr[2];
+  const long long total = 1 + B1 + B2;
+  K* epc = reinterpret_cast<K*>(g.ext_pc);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int line = t == 0 ? 0 : (t <= B1 ? 1 : 2);
+    const long long bi = t == 0 ? 0 : (line == 1 ? t - 1 : t - 1 - B1);
+    const long long nb_own = line == 0 ? 1 : (line == 1 ? B1 : B2);
+    const SumRec* own = g.sums[line];
+    const SumRec me = own[bi];
+    const unsigned long long k = me.key;
+    // best predecessor (key', rank') < (k, r) and successor > (k, r)
+    int prank = -1, srank = -1;
+    long long pidx = -1, sidx = -1;
+    unsigned long long pkey = 0, skey = 0;
+    auto better_pred = [&](unsigned long long kk, int rr) {
+      return prank < 0 || kk > pkey || (kk == pkey && rr > prank);
+    };
+    auto better_succ = [&](unsigned long long kk, int rr) {
+      return srank < 0 || kk < skey || (kk == skey && rr < srank);
+    };
+    if (bi > 0) {
+      prank = g.rank;
+      pidx = bi - 1;
+      pkey = own[bi - 1].key;
+    }
+    if (bi + 1 < nb_own) {
+      srank = g.rank;
+      sidx = bi + 1;
+      skey = own[bi + 1].key;
+    }
+    for (int s = 0; s < g.world; ++s) {
+      if (s == g.rank) continue;
+      const SumRec* a = g.peer_sums[s][line];
+      const long long m = g.peer_hdr[s][line];
+      if (m <= 0) continue;
+      // pred: s < r -> largest key' <= k; s > r -> largest key' < k
+      const long long pp = bsearch_key(a, m, k, s < g.rank) - 1;
+      if (pp >= 0) {
+        const unsigned long long kk = a[pp].key;
+        if (better_pred(kk, s)) {
+          prank = s;
+          pidx = pp;
+          pkey = kk;
+        }
+      }
+      // succ: s > r -> smallest key' >= k; s < r -> smallest key' > k
+      const long long ss = bsearch_key(a, m, k, s < g.rank);
+      if (ss < m) {
+        const unsigned long long kk = a[ss].key;
+        if (better_succ(kk, s)) {
+          srank = s;
+          sidx = ss;
+          skey = kk;
+        }
+      }
+    }
+    int pred = -1, succ = -1;
+    if (prank == g.rank) {
+      pred = own[pidx].llid;
+    } else if (prank >= 0) {
+      const SumRec& o = g.peer_sums[prank][line][pidx];
+      const int64_t h = g.n_own + 2 * t;
+      epc[h] = (K)o.lpc;
+      g.ext_gidx[h] = (uint32_t)o.lgid;
+      g.ext_pos[h] = o.lrow;
+      pred = (int)h;
+    }
+    if (srank == g.rank) {
+      succ = own[sidx].flid;
+    } else if (srank >= 0) {
+      const SumRec& o = g.peer_sums[srank][line][sidx];
+      const int64_t h = g.n_own + 2 * t + 1;
+      epc[h] = (K)o.fpc;
+      g.ext_gidx[h] = (uint32_t)o.fgid;
+      g.ext_pos[h] = o.frow;
+      succ = (int)h;
+    }
+    cand[(int64_t)line * g.n_own + me.flid].x = pred;
+    cand[(int64_t)line * g.n_own + me.llid].y = succ;
+  }
+}
+
+__global__ void k_iota_u32(uint32_t* __restrict__ out, int64_t n, int64_t base) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = (uint32_t)(base + i);
+}
+
+template <typename K>
+static int slab_own_impl(fgbd_ctx* ctx, SlabGC& g) {
+  const int64_t n = g.n_own;
+  const int b = g.b;
+  const int passes = (3 * b + 7) / 8;
+  int rc = run_sort<K, true>(ctx, n, b, 3, passes, nullptr);
+  if (rc) return rc;
+  ctx->rowid = ctx->perm[0];
+  {
+    dim3 grid(grid_for(n, 1 << 20), 3);
+    k_neighbors<<<grid, kBlock, 0, ctx->stream>>>(ctx->perm[0], ctx->perm[1], ctx->perm[2], n,
+                                                  ctx->cand, g.ext_pos, ctx->ctl, g.lo);
+    FGBD_LAUNCH(ctx);
+  }
+  // own packed coordinates into the extended array (halo records follow them)
+  FGBD_CUDA(ctx, cudaMemcpyAsync(g.ext_pc, ctx->pc, (size_t)n * sizeof(K), cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+  const int tiles = (int)((n + kBlkTile - 1) / kBlkTile);
+  const K* pc = (const K*)ctx->pc;
+  k_blk_count<K><<<dim3(tiles, 2), kBlock, 0, ctx->stream>>>(ctx->perm[1], ctx->perm[2], pc, n, b,
+                                                             g.tile_cnt, tiles);
+  FGBD_LAUNCH(ctx);
+  k_blk_scan<<<1, 32, 0, ctx->stream>>>(g.tile_cnt, tiles, g.hdr);
+  FGBD_LAUNCH(ctx);
+  k_blk_emit<K><<<dim3(tiles, 2), kBlock, 0, ctx->stream>>>(
+      ctx->perm[0], ctx->perm[1], ctx->perm[2], pc, n, b, g.tile_cnt, tiles, g.ext_gidx,
+      g.ext_pos, g.sums[0], g.sums[1], g.sums[2]);
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+int launch_graph_slab_own(fgbd_ctx* ctx, SlabGC& g) {
+  if (g.n_own < 1) return set_error(ctx, FGBD_E_ARG, "a slab rank needs at least one point");
+  int rc = (3 * g.b <= 32) ? slab_own_impl<uint32_t>(ctx, g)
+                           : slab_own_impl<unsigned long long>(ctx, g);
+  if (rc) return rc;
+  ctx->g_reordered = 1;
+  ctx->g_n = -1;  // not a stage-API graph
+  ctx->g_bits = g.b;
+  ctx->g_have_weights = 0;
+  ctx->g_have_noise = 0;
+  ctx->held_valid = 0;
+  return FGBD_OK;
+}
+
+template <typename K>
+static int slab_rows_impl(fgbd_ctx* ctx, SlabGC& g) {
+  const int64_t n = g.n_own;
+  const int rgrid = grid_for(1 + 2 * g.blk_cap, ctx->num_sms * 8);
+  k_resolve<K><<<rgrid, kBlock, 0, ctx->stream>>>(g, ctx->cand);
+  FGBD_LAUNCH(ctx);
+  const int grid = grid_for(n, kRowsGrid);
+  k_rows<K, false, true><<<grid, kBlock, 0, ctx->stream>>>(
+      ctx->cand, (const K*)g.ext_pc, n, g.b, g.ext_pos, ctx->rowid, EllRef{ctx->nbr, ctx->pay},
+      ctx->meta, ctx->partials, ctx->ctl, RowsSlab{g.ext_gidx, g.lo});
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+int launch_graph_slab_rows(fgbd_ctx* ctx, SlabGC& g) {
+  if (g.b > 15)
+    return set_error(ctx, FGBD_E_ARG, "slab partition supports bit depths up to 15");
+  return (3 * g.b <= 32) ? slab_rows_impl<uint32_t>(ctx, g)
+                         : slab_rows_impl<unsigned long long>(ctx, g);
+}
+
+int launch_weights_slab(fgbd_ctx* ctx, const SlabGC& g) {
+  const int grid = grid_for(g.n_own, ctx->num_sms * 8);
+  if (3 * g.b <= 32)
+    k_weights<uint32_t, false, false><<<grid, kBlock, 0, ctx->stream>>>(
+        EllRef{ctx->nbr, ctx->pay}, nullptr, (const uint32_t*)g.ext_pc, g.n_own, g.b, nullptr,
+        ctx->ctl, g.lo);
+  else
+    k_weights<unsigned long long, false, false><<<grid, kBlock, 0, ctx->stream>>>(
+        EllRef{ctx->nbr, ctx->pay}, nullptr, (const unsigned long long*)g.ext_pc, g.n_own, g.b,
+        nullptr, ctx->ctl, g.lo);
+  FGBD_LAUNCH(ctx);
+  ctx->g_have_weights = 1;
+  ctx->g_weights64 = 0;
+  return FGBD_OK;
+}
+
+int launch_iota_u32(fgbd_ctx* ctx, uint32_t* out, int64_t n, int64_t base) {
+  k_iota_u32<<<grid_for(n, ctx->num_sms * 8), kBlock, 0, ctx->stream>>>(out, n, base);
+  FGBD_LAUNCH(ctx);
   return FGBD_OK;
 }
 

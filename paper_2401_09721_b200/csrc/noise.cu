@@ -153,17 +153,30 @@ __device__ __forceinline__ double patch_std(const double4 (&v)[7], int c, int D,
   return __dsqrt_rn(div_rcp(var, (double)D, rD));
 }
 
-template <bool WEIGHTS>
+// SLAB: the rows are a slab rank's own rows, ELL words hold GLOBAL rows and
+// neighbour colours come from their owner's buffer (peer memory) via `sv`.
+__device__ __forceinline__ const double4* slab_row(const SlabView& sv, int64_t j) {
+  int r = sv.self;
+  if (j < sv.lo[r] || j >= sv.lo[r + 1]) {
+    r = 0;
+#pragma unroll 1
+    while (r + 1 < sv.world && j >= sv.lo[r + 1]) ++r;
+  }
+  return sv.y[r] + j;
+}
+
 #ifndef FGBD_NE_MINB
 #define FGBD_NE_MINB 6
 #endif
+template <bool WEIGHTS, bool SLAB = false>
 __global__ void __launch_bounds__(kNe2Warps * 32, FGBD_NE_MINB) k_noise2(const uint32_t* __restrict__ meta,
                                                            EllRef ell,
                                                            const double4* __restrict__ colors,
                                                            int64_t n, int D,
                                                            const Ctl* __restrict__ ctl,
                                                            double* __restrict__ fslr,
-                                                           double* __restrict__ part) {
+                                                           double* __restrict__ part,
+                                                           SlabView sv = SlabView{}) {
   __shared__ double s_rows[kNe2Warps][32 * kRowStride];
   __shared__ double s_acc[kNe2Warps][3][kGram];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -183,6 +196,7 @@ __global__ void __launch_bounds__(kNe2Warps * 32, FGBD_NE_MINB) k_noise2(const u
   for (int64_t chk = (int64_t)blockIdx.x * kNe2Warps + warp; chk < nchunks; chk += wstride) {
     const int64_t i = chk * 32 + lane;
     const bool valid = i < n;
+    const int64_t gi = SLAB ? sv.lo[sv.self] + i : i;  // the own row's (global) row number
     uint32_t mt = 0;
     int nb[kSlots];
     double4 v[7];
@@ -202,14 +216,14 @@ __global__ void __launch_bounds__(kNe2Warps * 32, FGBD_NE_MINB) k_noise2(const u
                                    : __ddiv_rn(-(double)(uint32_t)pr.y, sg2);
           const double q1 = sg_rcp ? div_rcp(-(double)(uint32_t)pr.w, sg2, rsg2)
                                    : __ddiv_rn(-(double)(uint32_t)pr.w, sg2);
-          const double w0 = nb[s] != (int)i ? exp(q0) : 0.0;
-          const double w1 = nb[s + 1] != (int)i ? exp(q1) : 0.0;
+          const double w0 = nb[s] != (int)gi ? exp(q0) : 0.0;
+          const double w1 = nb[s + 1] != (int)gi ? exp(q1) : 0.0;
           pr.y = __float_as_int((float)w0);
           pr.w = __float_as_int((float)w1);
           *reinterpret_cast<int4*>(ell.nbr + eslot(s, n, i)) = pr;
         }
       }
-      v[0] = ld_row(colors + i);
+      v[0] = SLAB ? ld_row(sv.y[sv.self] + gi) : ld_row(colors + i);
     }
     const int deg = (int)(mt & 7u);
     const bool ok = valid && deg >= D - 1;
@@ -221,8 +235,8 @@ __global__ void __launch_bounds__(kNe2Warps * 32, FGBD_NE_MINB) k_noise2(const u
           int j = nb[0];
 #pragma unroll
           for (int t = 1; t < kSlots; ++t) j = (s == t) ? nb[t] : j;
-          FGBD_DCHECK(j >= 0 && j < n);
-          v[r] = ld_row(colors + j);
+          FGBD_DCHECK(SLAB || (j >= 0 && j < n));
+          v[r] = SLAB ? ld_row(slab_row(sv, j)) : ld_row(colors + j);
         }
       }
     }
@@ -299,6 +313,21 @@ int launch_noise(fgbd_ctx* ctx, int64_t n, int patch, int fuse_weights) {
   FGBD_LAUNCH(ctx);
   k_reduce_cols<<<kNeVals, kBlock, 0, ctx->stream>>>(ctx->partials, grid, ctx->ctl);
   FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+int launch_noise_slab(fgbd_ctx* ctx, int64_t n, int patch, const SlabView& v) {
+  const int64_t nchunks = (n + 31) / 32;
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((nchunks + kNe2Warps - 1) / kNe2Warps, ctx->num_sms * 12));
+  k_noise2<true, true><<<grid, kNe2Warps * 32, 0, ctx->stream>>>(
+      ctx->meta, EllRef{ctx->nbr, ctx->pay}, nullptr, n, patch, ctx->ctl, ctx->fslr, ctx->partials,
+      v);
+  FGBD_LAUNCH(ctx);
+  k_reduce_cols<<<kNeVals, kBlock, 0, ctx->stream>>>(ctx->partials, grid, ctx->ctl);
+  FGBD_LAUNCH(ctx);
+  ctx->g_have_weights = 1;
+  ctx->g_weights64 = 0;
   return FGBD_OK;
 }
 

@@ -310,6 +310,29 @@ def test_slab_partition_bit_identical(gpu_ready, name, ranks):
                                    atol=CRIT_ATOL)
 
 
+@pytest.mark.parametrize("ranks", [2, 5])
+def test_slab_partition_any_point_order(gpu_ready, ranks):
+    """Shuffled input (the partition gathers each rank's points) with
+    duplicate points: still the single-GPU colours bit for bit."""
+    from paper_2401_09721_b200.slab import denoise_slab
+
+    clean, _ = fb.generate_cloud("two-tone", 60_000, seed=0)
+    noisy = fb.add_gaussian_noise(clean, 15.0, seed=4)
+    rng = np.random.default_rng(9)
+    p = rng.permutation(60_000)
+    g, y = np.array(noisy.coords)[p], np.array(noisy.colors)[p]
+    g[:50] = g[50]  # duplicates of one point, scattered in the input order
+    pc = fb.PointCloud(g, y, noisy.bit_depth)
+    a, ra = fb.denoise(pc)
+    b, rb = denoise_slab(pc, emulate_ranks=ranks)
+    assert rb.selected_q == ra.selected_q and rb.device["steps"] == ra.device["steps"]
+    assert rb.device["sigma_g"] == ra.device["sigma_g"]
+    assert rb.device["n_edges"] == ra.device["n_edges"]
+    assert np.array_equal(a.colors, b.colors)
+    ref = O.denoise(pc.coords, pc.colors, pc.bit_depth)
+    assert rb.selected_q == ref.selected_q
+
+
 @pytest.mark.slow
 def test_slab_partition_full_size(gpu_ready):
     from paper_2401_09721_b200.slab import denoise_slab

@@ -114,13 +114,18 @@ def test_two_rank_gloo_matches_single_process():
 def _handle_worker(rank, world, port, outdir):
     import torch.distributed as dist
 
-    from paper_2401_09721_b200.slab import exchange_handles, slab_bounds
+    from paper_2401_09721_b200.slab import exchange_handles, slab_partition
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     got = exchange_handles(bytes([rank]) * 64, dist.group.WORLD)
+    # every rank derives the same z-slab partition from the same frame
+    clean, _ = fb.generate_cloud("ramp", 30_000, seed=0)
+    g = np.array(clean.coords)[np.random.default_rng(3).permutation(30_000)]
+    part = slab_partition(fb.PointCloud(g, np.zeros(g.shape), clean.bit_depth), world)
+    own = part.own_index(rank)
     with open(os.path.join(outdir, f"h{rank}.pkl"), "wb") as fh:
-        pickle.dump((got, slab_bounds(1_000_003, world)), fh)
+        pickle.dump((got, part.counts.tolist(), part.zcut.tolist(), own), fh)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -132,16 +137,8 @@ def test_slab_handle_exchange_gloo():
         mp.start_processes(_handle_worker, args=(2, _free_port(), d), nprocs=2, join=True,
                            start_method="spawn")
         res = [pickle.load(open(os.path.join(d, f"h{r}.pkl"), "rb")) for r in range(2)]
-    for got, bounds in res:
+    for got, counts, zcut, _ in res:
         assert got == [bytes([0]) * 64, bytes([1]) * 64]
-        assert bounds == res[0][1] and bounds[0] == 0 and bounds[-1] == 1_000_003
-
-
-@pytest.mark.parametrize("n,world", [(10, 3), (1_000_000, 8), (7, 7), (8_000_000, 5)])
-def test_slab_bounds_partition(n, world):
-    from paper_2401_09721_b200.slab import slab_bounds
-
-    b = slab_bounds(n, world)
-    assert b[0] == 0 and b[-1] == n and all(b[i] <= b[i + 1] for i in range(world))
-    sizes = np.diff(b)
-    assert sizes.max() - sizes.min() <= 1
+        assert counts == res[0][1] and zcut == res[0][2] and sum(counts) == 30_000
+    own = np.concatenate([res[0][3], res[1][3]])
+    assert np.array_equal(np.sort(own), np.arange(30_000))  # the ranks' points partition the frame
