@@ -422,6 +422,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
     return nullptr;
   }
   ctx->num_sms = prop.multiProcessorCount;
+  ctx->l2_bytes = prop.l2CacheSize;
   if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(e, "stream");
   if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess)

@@ -163,7 +163,9 @@ struct fgbd_ctx {
   int coop_blocks[64] = {};     // co-resident grid of each persistent instantiation
   int lf_shape = 0;             // persistent kernel block shape (FGBD_LF_SHAPE)
   int lf_halo = 128;            // FGBD_LF_HALO: window rows either side of a TMA tile
-  int lf_chunk = 1;             // FGBD_LF_CHUNK: contiguous row range per block (0 = grid-stride)
+  int lf_chunk = -1;            // FGBD_LF_CHUNK: contiguous row range per block (0 = grid-stride,
+                                //   -1 = auto: contiguous while 3 signal buffers fit in L2)
+  int64_t l2_bytes = 0;         // device L2 capacity
   int reorder_rows = 1;         // FGBD_REORDER: denoise-path rows in scan-line-1 order
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
@@ -286,6 +288,8 @@ int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_ma
 int launch_mask_slab(fgbd_ctx* ctx, int64_t n_own, const double4* y, double sigma_est,
                      int active);
 int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64);
+// persistent filter: contiguous row range per block (true) or grid-stride waves
+bool lf_contiguous(const fgbd_ctx* ctx, int64_t rows);
 int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf);
 int launch_csr_steps(fgbd_ctx* ctx, const int64_t* d_indptr, const int64_t* d_indices,
                      const double* d_w, int64_t n, const double* d_in, double* d_tmp,

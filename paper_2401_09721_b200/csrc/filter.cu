@@ -1069,6 +1069,20 @@ static StepArgs step_args(fgbd_ctx* ctx, int64_t n) {
   return a;
 }
 
+}  // namespace fgbd
+
+// Rows per block: a contiguous range (the graph streams in long runs, and
+// rows a slice apart stay in L2 because the whole signal does) while the
+// three signal buffers fit in L2; otherwise grid-stride waves, so a row's
+// neighbours one z-slice away (k^2 rows) are read by concurrently running
+// blocks and hit L2 (8M lattice: 13.7 -> 9.6 ms for 64 steps).
+bool fgbd::lf_contiguous(const fgbd_ctx* ctx, int64_t rows) {
+  if (ctx->lf_chunk >= 0) return ctx->lf_chunk != 0;
+  return (double)rows * 32.0 * 3.0 <= (double)ctx->l2_bytes;
+}
+
+namespace fgbd {
+
 template <int WM, bool SELECT, int BLK, int MINB, bool TMA = false, bool P2P = false>
 static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
   auto kern = k_lf_run<WM, SELECT, BLK, MINB, TMA, P2P>;
@@ -1089,7 +1103,8 @@ static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
   const int grid = (int)std::max<int64_t>(
       1, std::min<int64_t>(std::min<int64_t>((a.n + BLK - 1) / BLK, ctx->coop_blocks[slot]),
                            kMaxCoopBlocks));
-  a.chunk = (TMA || P2P || ctx->lf_chunk) ? ((a.n + grid - 1) / grid + BLK - 1) / BLK * BLK : 0;
+  a.chunk = (TMA || P2P || lf_contiguous(ctx, a.n)) ? ((a.n + grid - 1) / grid + BLK - 1) / BLK * BLK
+                                                     : 0;
   a.halo = std::min(ctx->lf_halo, kHaloMax);
   if (P2P) {
     if (!ctx->p2p_flags) {

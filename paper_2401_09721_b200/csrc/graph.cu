@@ -565,6 +565,8 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
       const unsigned long long e = (unsigned long long)cnt;
       ctl->n_edges = e;
       ctl->sigma_g = e ? fx52_to_double(a) / (double)e : 0.0;
+      ctl->sg_fx[0] = (unsigned long long)a;  // a slab rank's share (all-gathered)
+      ctl->sg_fx[1] = (unsigned long long)(a >> 64);
       ctl->ticket[0] = 0;
     }
   }

@@ -192,6 +192,7 @@ struct SlabArgs {
   unsigned long long epoch;  // frame epoch: step ticks are epoch << 32 | step
   int fixed_steps;           // cached path when > 0 (no criterion)
   int select;
+  int contiguous;            // rows per block: contiguous range (1) or grid-stride waves (0)
 };
 
 // Barrier over the bpg co-resident blocks of one group (sense-reversing).
@@ -276,8 +277,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
       // prefetched; gathers are branch-free (padding = own row, w = 0) and
       // only rows outside [lo, hi) look up their owner's (peer) buffer
       const double4* own_in = a.bufs[r][ib];
-      int64_t i = (int64_t)lb * chunk + threadIdx.x;  // own (local) row
-      const int64_t end = min(n_own, (int64_t)(lb + 1) * chunk);
+      // own (local) rows: a contiguous share, or grid-stride waves when the
+      // signals do not fit in L2 (see fgbd::lf_contiguous)
+      int64_t i = a.contiguous ? (int64_t)lb * chunk + threadIdx.x
+                               : (int64_t)lb * blockDim.x + threadIdx.x;
+      const int64_t end = a.contiguous ? min(n_own, (int64_t)(lb + 1) * chunk) : n_own;
+      const int64_t rstep = a.contiguous ? (int64_t)blockDim.x : (int64_t)a.bpg * blockDim.x;
       int nbn[kSlots];
       float wn[kSlots];
       auto load_slots = [&](int64_t row, int (&nb)[kSlots], float (&w)[kSlots]) {
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
           nb[s] = nbn[s];
           w[s] = wn[s];
         }
-        const int64_t inext = i + blockDim.x;
+        const int64_t inext = i + rstep;
         if (inext < end) load_slots(inext, nbn, wn);
         const int64_t gi = lo + i;
         const double4 f = ld_row_hint(own_in + gi, pol_keep);
@@ -775,6 +780,9 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
     for (int g = 0; g < s->groups; ++g) max_rows = std::max(max_rows, s->loc[g].g.n_own);
     a.bpg = (int)std::max<int64_t>(
         1, std::min<int64_t>(capacity / s->groups, (max_rows + kBlock - 1) / kBlock));
+    int64_t rows_here = 0;  // signal rows resident on this GPU
+    for (int g = 0; g < s->groups; ++g) rows_here += s->loc[g].g.n_own;
+    a.contiguous = lf_contiguous(parent, rows_here) ? 1 : 0;
     FGBD_CUDA(parent,
               cudaMemsetAsync(s->gbar, 0, 2 * s->groups * sizeof(unsigned), parent->stream));
     void* args[] = {&a};
