@@ -66,6 +66,9 @@ def parse():
                     help="slab workload at N=1: logical ranks emulated on the one GPU")
     ap.add_argument("--workers", type=int, default=None,
                     help="host threads per GPU (default: video 3, ply 2)")
+    ap.add_argument("--static-geometry", action="store_true",
+                    help="video: the caller vouches that frames share coordinates "
+                         "(FGBD_FLAG_STATIC_GEOMETRY: colours-only uploads)")
     ap.add_argument("--no-reuse", action="store_true",
                     help="video/ply: rebuild the graph of every frame even when the geometry is static")
     return ap.parse_args()
@@ -522,10 +525,10 @@ def run_video(args):
     # a pool of distinct noisy frames in pinned memory, cycled over the video
     clean, _ = fb.generate_cloud(args.kind, args.n, seed=0)
     pool = []
+    c = nat.pinned_empty(clean.coords.shape, np.int64)  # one capture geometry
+    c[...] = clean.coords
     for s in range(8):
         noisy = fb.add_gaussian_noise(clean, args.sigma, seed=1 + s)
-        c = nat.pinned_empty(noisy.coords.shape, np.int64)
-        c[...] = noisy.coords
         y = nat.pinned_empty(noisy.colors.shape, np.float64)
         y[...] = noisy.colors
         pool.append(fb.PointCloud(c, y, noisy.bit_depth))
@@ -540,9 +543,9 @@ def run_video(args):
         compute.append(sum(rep.stage_timings.values()))
 
     # warm-up: contexts for every worker thread, pinned output pool
+    kw = dict(reuse_graph=not args.no_reuse, static_geometry=args.static_geometry)
     denoise_sequence(load, cfg, n_frames=min(2 * cfg.reestimate_interval, args.frames),
-                     workers=args.workers, process_group=pg, sink=sink,
-                     reuse_graph=not args.no_reuse)
+                     workers=args.workers, process_group=pg, sink=sink, **kw)
     if world > 1:
         import torch.distributed as dist
 
@@ -551,7 +554,7 @@ def run_video(args):
     compute.clear()
     t0 = time.perf_counter()
     res = denoise_sequence(load, cfg, n_frames=args.frames, workers=args.workers,
-                           process_group=pg, sink=sink, reuse_graph=not args.no_reuse)
+                           process_group=pg, sink=sink, **kw)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     if world > 1:
@@ -562,7 +565,13 @@ def run_video(args):
         wall = float(t.item())
     if rank == 0:
         heads = sum(1 for r in res.values() if not r[1].cached)
+        coords_b, colors_b = int(pool[0].coords.nbytes), int(pool[0].colors.nbytes)
+        h2d = colors_b + (0 if args.static_geometry else coords_b)
         print(json.dumps({
+            "e2e": {"h2d_bytes_per_step": h2d, "d2h_bytes_per_step": colors_b,
+                    "host_link_bytes_per_frame": h2d + colors_b,
+                    "note": "static geometry: coordinates go up once per worker"
+                            if args.static_geometry else "coordinates re-sent and compared on device"},
             "metric": f"frames/sec, {args.frames}-frame video at {args.n:,} pts/frame "
                       f"(K={cfg.reestimate_interval} q reuse, e2e from pinned host frames)",
             "value": args.frames / wall, "unit": "frames/s", "n_gpus": world,
@@ -574,7 +583,8 @@ def run_video(args):
                        "rank0_heads": heads, "rank0_frames": len(res),
                        "rank0_graph_reused": sum(1 for r in res.values()
                                                  if r[1].device and r[1].device.get("graph_reused")),
-                       "geometry": "static (frames share the clean cloud's coordinates)"},
+                       "geometry": "static (frames share the clean cloud's coordinates)",
+                       "static_geometry_flag": bool(args.static_geometry)},
         }), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -711,7 +721,7 @@ def run_slab(args):
 
     for _ in range(warmup_steps(args)):
         rep = step()
-    walls, devs, stages = [], [], []
+    walls, devs, stages, per_rank = [], [], [], []
     for _ in range(args.steps):
         if pg is not None:
             import torch.distributed as dist
@@ -724,6 +734,7 @@ def run_slab(args):
         stages.append((rep.device["t_h2d"], rep.stage_timings["graph_construction"],
                        rep.stage_timings["noise_estimation"], rep.device["t_lf_steps"],
                        rep.device["t_d2h"]))
+        per_rank.append(rep.device["slab_rank_seconds"])
     wall = float(np.sum(walls))
     if world > 1:
         import torch.distributed as dist
@@ -732,6 +743,7 @@ def run_slab(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wall = float(t.item())
     st = np.mean(np.array(stages), axis=0) * 1e3
+    pr = np.mean(np.array(per_rank), axis=0) * 1e3  # [rank][phase] ms
     if rank == 0:
         print(json.dumps({
             "metric": f"frames/sec, one {n:,}-point frame slab-partitioned over the GPUs",
@@ -739,9 +751,14 @@ def run_slab(args):
             "ms_per_step": 1e3 * wall / args.steps, "steps": args.steps,
             "higher_is_better": True, "scaling": "strong", "dtype": "f64", "data": "synthetic",
             "device_ms_rank0": 1e3 * float(np.mean(devs)),
-            "rank0_stage_ms": {"h2d_own_points": st[0], "graph_construction": st[1],
-                               "noise_estimation_and_mask": st[2], "lf_steps": st[3],
-                               "d2h_own_points": st[4]},
+            "stage_ms": {"h2d": st[0], "graph_construction": st[1],
+                         "noise_estimation_and_mask": st[2], "lf_steps": st[3], "d2h": st[4]},
+            # per slab rank (device events around that rank's own work):
+            # upload + own sort + block lists, cross-slab rows, NE + FSLR, output
+            "per_rank_ms": {"upload_sort_blocks": pr[:, 0].tolist(),
+                            "cross_slab_rows": pr[:, 1].tolist(),
+                            "ne_fslr": pr[:, 2].tolist(), "output_d2h": pr[:, 3].tolist(),
+                            "max_rank_gc_ne_h2d": float(np.max(pr[:, 0] + pr[:, 1] + pr[:, 2]))},
             "config": {"workload": "BASELINE.json configs[4]", "kind": args.kind, "n_points": n,
                        "sigma": args.sigma, "selected_q": rep.selected_q,
                        "filter_steps_S": rep.device["steps"], "slab_ranks": ranks,

@@ -59,6 +59,12 @@ enum {
  * rebuilding (the SLG is a pure function of the coordinates; the check is an
  * exact device-side comparison).  For static-geometry frame sequences. */
 #define FGBD_FLAG_REUSE_GRAPH  0x8u
+/* fgbd_denoise: the CALLER guarantees this frame's coordinates are the ones
+ * of the graph this context holds (same n and bit depth): the coordinates are
+ * neither uploaded nor compared, so a static-geometry frame moves only its
+ * colours over PCIe.  Without a held graph it behaves as REUSE_GRAPH.  A
+ * caller that breaks the guarantee gets the held graph's results. */
+#define FGBD_FLAG_STATIC_GEOMETRY 0x10u
 
 enum { FGBD_CRIT_POOLED = 0, FGBD_CRIT_PER_CHANNEL = 1 };   /* filtering.py:47 */
 enum { FGBD_TAU_COUNT = 0, FGBD_TAU_COUNT_PLUS_ONE = 1 };   /* filtering.py:49 */
@@ -119,6 +125,10 @@ typedef struct fgbd_report {
      "Jacobi did not converge" on such a matrix (noise.py:180-185); this
      build returns the eigenvalues */
   int32_t jacobi_direct_off[3];
+  /* slab ranks run by this call (fgbd_denoise_slab): per rank, seconds of
+     device time in [0] upload + own sort + block lists, [1] cross-slab
+     neighbours + rows, [2] NE-GBP + FSLR, [3] output + download */
+  double t_slab_rank[16][4];
 } fgbd_report;
 
 /* Result of NE-GBP (noise.py:63-73). */

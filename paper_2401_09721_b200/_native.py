@@ -27,6 +27,7 @@ FLAG_NO_TIMING = 0x4
 SLAB_EMULATED = 0x1
 SLAB_FULL_OUTPUT = 0x2
 FLAG_REUSE_GRAPH = 0x8
+FLAG_STATIC_GEOMETRY = 0x10
 MAX_PATCH = 7
 TRACE_MAX = 1025
 
@@ -57,7 +58,8 @@ class Report(C.Structure):
                 ("tail_tau", c_f64 * 3), ("tail_fallback", c_i32 * 3), ("n_trace", c_i32),
                 ("trace", c_f64 * TRACE_MAX), ("gpu_launches", c_i32),
                 ("t_lf_steps", c_f64), ("t_h2d", c_f64), ("t_d2h", c_f64),
-                ("graph_reused", c_i32), ("jacobi_direct_off", c_i32 * 3)]
+                ("graph_reused", c_i32), ("jacobi_direct_off", c_i32 * 3),
+                ("t_slab_rank", (c_f64 * 4) * 16)]
 
 
 class Noise(C.Structure):

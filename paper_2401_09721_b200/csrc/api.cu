@@ -550,9 +550,11 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   const int64_t* frame_coords = dev ? coords : ctx->coords64;
   // static-geometry reuse: the held graph stands if this frame's coordinates
   // are byte-identical to the ones it was built from (exact device compare)
-  const bool want_reuse = (flags & FGBD_FLAG_REUSE_GRAPH) && !w64;
+  const bool want_reuse = (flags & (FGBD_FLAG_REUSE_GRAPH | FGBD_FLAG_STATIC_GEOMETRY)) && !w64;
   const bool may_reuse = want_reuse && ctx->held_valid && ctx->g_n == n && ctx->g_bits == bits &&
                          ctx->g_have_weights && !ctx->g_weights64;
+  // the caller vouches for the geometry: no coordinate upload, no compare
+  const bool trusted = may_reuse && (flags & FGBD_FLAG_STATIC_GEOMETRY);
   // A frame that will probably reuse the graph has no build for the colour
   // upload to hide behind, so its colours travel ahead of the device lock,
   // together with the coordinates.  Both copies go before the compare
@@ -560,14 +562,17 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   // wait for another context's persistent filter to release the SMs.
   const double* frame_colors = colors;
   bool colors_dev = dev;
-  if (!dev && (rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false))) return rc;
+  if (!dev && !trusted && (rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false)))
+    return rc;
   if (may_reuse && !dev) {
     if ((rc = h2d(ctx, ctx->out, colors, 3 * n * sizeof(double), false))) return rc;
     frame_colors = ctx->out;
     colors_dev = true;
   }
   bool reuse = false;
-  if (may_reuse) {
+  if (trusted) {
+    reuse = true;
+  } else if (may_reuse) {
     int same = 0;  // syncs the stream: coordinates (and colours) have landed
     if ((rc = coords_equal(ctx, frame_coords, ctx->held_coords, 3 * n, &same))) return rc;
     reuse = same != 0;
@@ -590,7 +595,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   if (reuse) {
     if ((rc = reset_ctl(ctx))) return rc;
     if ((rc = restore_graph_header(ctx))) return rc;
-    ctx->cur_coords = frame_coords;
+    ctx->cur_coords = trusted ? ctx->held_coords : frame_coords;
   } else {
     if ((rc = stage_graph(ctx, frame_coords, n, bits, true, w64, !fuse_w, ctx->reorder_rows != 0)))
       return rc;

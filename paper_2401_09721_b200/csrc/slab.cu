@@ -517,6 +517,7 @@ struct fgbd_slab {
   double* part = nullptr;
   int bpg_cap = 0;
   unsigned long long epoch = 1;
+  cudaEvent_t rev[kMaxRanks][10] = {};  // per local rank: start/end of its phases
 };
 
 namespace {
@@ -643,6 +644,7 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
     const int64_t n_own = counts[r];
     int rc = ensure_capacity(ctx, n_own, 3 * b > 32);
     if (rc) return set_error(parent, rc, ctx->err);
+    if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][0], ctx->stream));
     FGBD_CUDA(parent, cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
     SlabGC& G = lc.g;
     G.world = P;
@@ -674,6 +676,7 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
     k_slab_expand<<<ctx->num_sms * 8, kBlock, 0, ctx->stream>>>(ctx->out, n_own, ybuf, lo[r],
                                                                 ctx->rowid);
     FGBD_LAUNCH(ctx);
+    if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][1], ctx->stream));
     off += n_own;
   }
   FinArgs fin{};
@@ -682,7 +685,9 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
   // ---- phase 2: cross-slab neighbours, rows, sigma_g -------------------------
   for (int g = 0; g < s->groups; ++g) {
     auto& lc = s->loc[g];
+    if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][2], lc.ctx->stream));
     if (int rc = launch_graph_slab_rows(lc.ctx, lc.g)) return set_error(parent, rc, lc.ctx->err);
+    if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][3], lc.ctx->stream));
   }
   if (int rc = all_gather(parent, s, ST_SIGMA, fin)) return rc;
   for (int g = 0; g < s->groups; ++g)
@@ -721,8 +726,10 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
                                                  std::to_string(1 + maxdeg) + ") of this graph");
     for (int g = 0; g < s->groups; ++g) {
       auto& lc = s->loc[g];
+      if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][4], lc.ctx->stream));
       if (int rc = launch_noise_slab(lc.ctx, lc.g.n_own, D, view_of(lc.g.rank)))
         return set_error(parent, rc, lc.ctx->err);
+      if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][5], lc.ctx->stream));
     }
     if (int rc = all_gather(parent, s, ST_NOISE, fin)) return rc;
     for (int g = 0; g < s->groups; ++g) {
@@ -736,8 +743,10 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
     for (int g = 0; g < s->groups; ++g) {
       auto& lc = s->loc[g];
       const double4* y = at<double4>(s->base[lc.g.rank], s->L.bufs[BUF_Y]);
+      if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][8], lc.ctx->stream));
       if (int rc = launch_mask_slab(lc.ctx, lc.g.n_own, y, sig, active))
         return set_error(parent, rc, lc.ctx->err);
+      if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][9], lc.ctx->stream));
     }
     fin.active = active;
     fin.q_max = cfg->q_max;
@@ -796,6 +805,7 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
   for (int g = 0; g < s->groups; ++g) {
     auto& lc = s->loc[g];
     const int r = lc.g.rank;
+    if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][6], lc.ctx->stream));
     OutArgs o{};
     for (int k = 0; k < 3; ++k) o.bufs[k] = at<double4>(s->base[r], s->L.bufs[k]) - lo[r];
     o.ctl = lc.ctx->ctl;
@@ -812,6 +822,7 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
     if (!s->full)
       FGBD_CUDA(parent, cudaMemcpyAsync(out_colors + 3 * off, lc.ctx->out, (size_t)lc.g.n_own * 24,
                                         cudaMemcpyDefault, lc.ctx->stream));
+    if (timing) FGBD_CUDA(parent, cudaEventRecord(s->rev[g][7], lc.ctx->stream));
     off += lc.g.n_own;
   }
   if (s->full) {
@@ -874,6 +885,15 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
     rep->t_lf_steps = ev_sec(ev[3], ev[6]);
     rep->t_h2d = ev_sec(ev[0], ev[1]);
     rep->t_d2h = ev_sec(ev[4], ev[5]);
+    for (int g = 0; g < s->groups; ++g) {
+      const int r = s->loc[g].g.rank;
+      rep->t_slab_rank[r][0] = ev_sec(s->rev[g][0], s->rev[g][1]);
+      rep->t_slab_rank[r][1] = ev_sec(s->rev[g][2], s->rev[g][3]);
+      rep->t_slab_rank[r][2] = cached_q >= 0 ? 0.0
+                                             : ev_sec(s->rev[g][4], s->rev[g][5]) +
+                                                   ev_sec(s->rev[g][8], s->rev[g][9]);
+      rep->t_slab_rank[r][3] = ev_sec(s->rev[g][6], s->rev[g][7]);
+    }
   }
   return FGBD_OK;
 }
@@ -926,6 +946,12 @@ fgbd_slab* fgbd_slab_create(fgbd_ctx* ctx, int32_t world, int32_t rank, int64_t 
     if (alloc_local(ctx, s, g) != FGBD_OK) return fail();
     s->base[lc.g.rank] = (char*)lc.region;
   }
+  for (int g = 0; g < s->groups; ++g)
+    for (auto& e : s->rev[g])
+      if (cudaEventCreate(&e) != cudaSuccess) {
+        set_error(ctx, FGBD_E_CUDA, "slab event");
+        return fail();
+      }
   s->bpg_cap = ctx->num_sms * 4;
   if (cudaMalloc(&s->gbar, 2 * kMaxRanks * sizeof(unsigned)) != cudaSuccess ||
       cudaMemset(s->gbar, 0, 2 * kMaxRanks * sizeof(unsigned)) != cudaSuccess ||
@@ -956,6 +982,9 @@ void fgbd_slab_destroy(fgbd_ctx* ctx, fgbd_slab* s) {
   }
   if (s->gbar) cudaFree(s->gbar);
   if (s->part) cudaFree(s->part);
+  for (auto& row : s->rev)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
   delete s;
 }
 

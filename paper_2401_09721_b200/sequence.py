@@ -78,7 +78,7 @@ def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
                      cfg: FilterConfig = FilterConfig(), *, n_frames: int | None = None,
                      workers: int = 3, process_group=None, denoise_fn=None,
                      sink: Callable[[int, PointCloud, DenoiseReport], object] | None = None,
-                     reuse_graph: bool = True,
+                     reuse_graph: bool = True, static_geometry: bool = False,
                      ) -> dict[int, tuple[PointCloud, DenoiseReport]]:
     """Denoise a frame sequence with the reference's every-K-frames q reuse.
 
@@ -92,10 +92,15 @@ def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
     With `reuse_graph` (default), a frame whose coordinates are byte-identical
     to the previous frame of the same worker reuses that worker's scan-line
     graph (static geometry; checked exactly on the device, results
-    unchanged; `report.device["graph_reused"]`).
+    unchanged; `report.device["graph_reused"]`).  With `static_geometry`
+    the caller guarantees every frame has the same coordinates (e.g. one
+    capture rig, colours re-measured): after a worker's first frame its
+    coordinates are neither uploaded nor compared, halving the per-frame
+    host->device bytes (FGBD_FLAG_STATIC_GEOMETRY).
     """
     if denoise_fn is None:
-        denoise_fn = partial(denoise_frame, reuse_graph=reuse_graph)
+        denoise_fn = partial(denoise_frame, reuse_graph=reuse_graph,
+                             static_geometry=static_geometry)
     load = frames if callable(frames) else (lambda i: frames[i])
     n = n_frames if n_frames is not None else len(frames)  # type: ignore[arg-type]
     world, rank = 1, 0

@@ -243,6 +243,10 @@ def _report(rep, cfg, cached_q, cached_sigma_est, world) -> DenoiseReport:
                "low_pass_filter": float(rep.t_low_pass_filter)}
     info = _device_info(rep, cfg.patch_size)
     info["slab_ranks"] = world
+    # per rank run here: device seconds of [upload + own sort + block lists,
+    # cross-slab neighbours + rows, NE-GBP + FSLR, output + download]
+    info["slab_rank_seconds"] = [[float(rep.t_slab_rank[r][k]) for k in range(4)]
+                                 for r in range(world)]
     if cached_q is None:
         if rep.all_excluded_fallback:
             warnings.warn("variance mask excluded every point; selecting unmasked")

@@ -96,3 +96,35 @@ def test_ply_reuse(gpu_ready):
     assert [r.device["graph_reused"] for _, r in outs] == [False, True, True]
     for (o, _), s in zip(outs, srcs):
         assert o == denoise_ply(s)[0]
+
+
+def test_static_geometry_skips_coordinates(gpu_ready):
+    """FGBD_FLAG_STATIC_GEOMETRY: the caller vouches for the geometry, so no
+    coordinate upload or compare -- results stay bit-identical; the first
+    frame (no held graph) builds it."""
+    fs = frames(k=4)
+    fresh = [fb.denoise(f) for f in fs]
+    got = [denoise_frame(f, static_geometry=True) for f in fs]
+    assert [r.device["graph_reused"] for _, r in got] == [False] + [True] * 3
+    for a, b in zip(got, fresh):
+        same(a, b)
+    # cached frames on the held graph
+    q, s = fresh[0][1].selected_q, fresh[0][1].sigma_est
+    plain = [fb.denoise(f, cached_q=q, cached_sigma_est=s) for f in fs]
+    denoise_frame(fs[0], static_geometry=True)
+    reused = [denoise_frame(f, cached_q=q, cached_sigma_est=s, static_geometry=True) for f in fs]
+    assert all(r.device["graph_reused"] for _, r in reused)
+    for a, b in zip(reused, plain):
+        same(a, b)
+
+
+def test_sequence_static_geometry(gpu_ready):
+    from paper_2401_09721_b200.sequence import denoise_sequence
+
+    fs = frames(k=7)
+    cfg = fb.FilterConfig(reestimate_interval=3)
+    a = denoise_sequence(fs, cfg, workers=2, static_geometry=True)
+    b = denoise_sequence(fs, cfg, workers=1, reuse_graph=False)
+    for f in range(7):
+        assert np.array_equal(a[f][0].colors, b[f][0].colors)
+        assert a[f][1].selected_q == b[f][1].selected_q
