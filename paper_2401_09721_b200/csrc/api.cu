@@ -518,6 +518,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
                      int32_t bits, const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
                      double* out_colors, fgbd_report* rep, uint32_t flags) {
   if (!ctx || !rep) return set_error(ctx, FGBD_E_ARG, "null context or report");
+  NvtxRange nv_frame("fgbd.denoise");
   cudaSetDevice(ctx->device);
   ctx->err.clear();
   ctx->launches = 0;
@@ -597,6 +598,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = restore_graph_header(ctx))) return rc;
     ctx->cur_coords = trusted ? ctx->held_coords : frame_coords;
   } else {
+    NvtxRange nv("fgbd.graph");
     if ((rc = stage_graph(ctx, frame_coords, n, bits, true, w64, !fuse_w, ctx->reorder_rows != 0)))
       return rc;
     if (want_reuse && (rc = hold_coords(ctx, frame_coords, n))) return rc;
@@ -617,6 +619,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = launch_compact(ctx, n, fin, dev ? out_colors : ctx->out, 1))) return rc;
   } else {
     const int D = cfg->patch_size;
+    NvtxRange nv("fgbd.noise+filter");
     if ((rc = launch_noise(ctx, n, D, fuse_w ? 1 : 0))) return rc;
     if (fuse_w) {
       ctx->g_have_weights = 1;
@@ -645,6 +648,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   device_last_compute(ctx->device) = ctx->ev_done;
   if (!ctx->async_lock || cached_q < 0) FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_done));
   compute_lock.unlock();
+  NvtxRange nv_out("fgbd.download");
   if (!dev && (rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), false))) return rc;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
   if ((rc = pull_ctl(ctx))) return rc;

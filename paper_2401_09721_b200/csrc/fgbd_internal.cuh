@@ -19,6 +19,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <string>
@@ -230,6 +231,15 @@ int cuda_error(fgbd_ctx* ctx, cudaError_t e, const char* where);
     cudaError_t e__ = cudaGetLastError();                      \
     if (e__ != cudaSuccess) return fgbd::cuda_error(ctx, e__, "kernel launch"); \
   } while (0)
+
+// NVTX range over a host scope (the reference's per-stage timers,
+// filtering.py:277-300, as profiler ranges: fgbd.graph / fgbd.noise / ...)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64);
 int require_point_rows(fgbd_ctx* ctx);

@@ -1,11 +1,16 @@
 // Scan-line graph construction on sm_100a (reference graph.py:122-251).
 //
 //   k_prep       coords int64 -> packed line-1 code (pc) + digit histograms
-//                of all three scan lines for every radix pass (one read)
-//   k_onesweep   one stable LSD pass for all three lines: warp multisplit
-//                (per-bit ballots) -> decoupled look-back across tiles -> smem
-//                reorder -> coalesced scatter (8-bit digits, ceil(3b/8)
-//                passes, exactly the reference's pass count, graph.py:168)
+//                of every radix pass (one read); flags an input that is not
+//                already in scan-line-1 order
+//   k_onesweep   one stable LSD pass: warp multisplit (per-bit ballots) ->
+//                decoupled look-back across tiles -> smem reorder ->
+//                coalesced scatter (8-bit digits).  Line 1 takes ceil(3b/8)
+//                passes over its code (skipped when the input is already in
+//                line-1 order).  Lines 2 and 3 are DERIVED: a stable sort of
+//                the line-1 order by x alone is the (x, z, y, index) order of
+//                line 2, and a stable sort of that by y is line 3's (y, x, z,
+//                index) order -- ceil(b/8) passes each instead of ceil(3b/8).
 //   k_neighbors  rank neighbours: cand[l][perm_l[k]] = (perm_l[k-1], perm_l[k+1])
 //   k_rows       per point: sort + dedup <= 6 candidates (the reference's
 //                np.unique + lexsort, graph.py:188-208), exact squared
@@ -55,20 +60,32 @@ __device__ __forceinline__ void unpack(K pc, int b, long long* x, long long* y, 
   *z = (long long)(pc >> (2 * b));
 }
 
-// Histogram of every digit of every line, warp-aggregated smem atomics.
+constexpr int kFlagUnsorted = 16;  // Ctl::err_flags: input is not in scan-line-1 order
+
+// sort key of line l's pass p: line 0 its code; lines 1 / 2 (derived) the
+// x / y field of the line-1 code
+template <typename K>
+__device__ __forceinline__ K pass_key(K code, int line, int b) {
+  if (line == 0) return code;
+  const K m = (K(1) << b) - 1;
+  return line == 1 ? (code & m) : ((code >> b) & m);
+}
+
+// Histogram of every digit of every pass, warp-aggregated smem atomics.
+// hist layout [line][kMaxPasses][256]; line l has passes[l] passes.
 template <typename K, bool FROM_COORDS>
 __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coords,
                                                  const K* __restrict__ keys_in, int64_t n,
-                                                 int b, int nlines, int passes,
+                                                 int b, int nlines, int passes0, int passes12,
                                                  K* __restrict__ pc, uint32_t* __restrict__ hist,
                                                  Ctl* __restrict__ ctl) {
-  extern __shared__ uint32_t s_hist[];  // [nlines][passes][256]
-  const int nh = nlines * passes * kRadix;
+  extern __shared__ uint32_t s_hist[];  // [nlines][kMaxPasses][256]
+  const int nh = nlines * kMaxPasses * kRadix;
   for (int t = threadIdx.x; t < nh; t += blockDim.x) s_hist[t] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long lim = (1ll << b);
-  bool bad = false;
+  bool bad = false, unsorted = false;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
     const int64_t i = i0 + threadIdx.x;
@@ -84,9 +101,19 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
         code = keys_in[i];
       }
     }
+    if (FROM_COORDS) {
+      // an inversion with the next point: the input is not in line-1 order
+      K next = __shfl_down_sync(kFull, code, 1);
+      if (lane == 31 && i + 1 < n) {
+        const long long x = coords[3 * i + 3], y = coords[3 * i + 4], z = coords[3 * i + 5];
+        next = (K(z) << (2 * b)) | (K(y) << b) | K(x);
+      }
+      unsorted |= valid && i + 1 < n && next < code;
+    }
     const unsigned vmask = __ballot_sync(kFull, valid);
     for (int l = 0; l < nlines; ++l) {
-      const K key = FROM_COORDS ? line_key(code, l, b) : code;
+      const K key = FROM_COORDS ? pass_key(code, l, b) : code;
+      const int passes = l == 0 ? passes0 : passes12;
       for (int p = 0; p < passes; ++p) {
         const unsigned d = valid ? (unsigned)((key >> (8 * p)) & 0xff) : 0x100u;
         // a digit shared by the whole warp (raster-ordered input, high
@@ -94,14 +121,16 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
         // contend when equal digits are scattered across the warp
         const unsigned d0 = __shfl_sync(kFull, d, 0);
         if (__all_sync(kFull, d == d0) && d0 < 0x100u) {
-          if (lane == 0) atomicAdd(&s_hist[(l * passes + p) * kRadix + d0], (uint32_t)__popc(vmask));
+          if (lane == 0)
+            atomicAdd(&s_hist[(l * kMaxPasses + p) * kRadix + d0], (uint32_t)__popc(vmask));
         } else if (valid) {
-          atomicAdd(&s_hist[(l * passes + p) * kRadix + d], 1u);
+          atomicAdd(&s_hist[(l * kMaxPasses + p) * kRadix + d], 1u);
         }
       }
     }
   }
   if (bad) atomicOr(&ctl->err_flags, 1);
+  if (__any_sync(kFull, unsorted) && lane == 0) atomicOr(&ctl->err_flags, kFlagUnsorted);
   __syncthreads();
   for (int t = threadIdx.x; t < nh; t += blockDim.x)
     if (s_hist[t]) atomicAdd(&hist[t], s_hist[t]);
@@ -114,14 +143,17 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
 struct SortPass {
   const void* src_keys[3];      // null on pass 0 in SLG mode (keys from pc)
   const void* pc;
-  const uint32_t* src_vals[3];  // null on pass 0 (identity)
+  const uint32_t* src_vals[3];  // null on pass 0 (identity); a derived line's pass 0: the
+                                // previous line's order
   void* dst_keys[3];
   uint32_t* dst_vals[3];
-  const uint32_t* hist;         // [line][passes][256] digit counts (k_prep)
+  const uint32_t* hist;         // [line][kMaxPasses][256] digit counts (k_prep)
   unsigned long long* status;   // [line][tiles][256]
   unsigned int* tile_ctr;       // [line]
+  const Ctl* ctl;               // SLG line 0: skip when the input is already sorted
   int64_t n;
   int b, pass, passes, tiles;
+  int line0;                    // line of blockIdx.y == 0
   unsigned int epoch;
 };
 
@@ -161,8 +193,16 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   __shared__ uint32_t s_wsum[8], s_hsum[8];
   __shared__ int s_tile;
 
-  const int line = blockIdx.y;
+  const int line = p.line0 + blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (SLG && line == 0 && !(*(volatile const int*)&p.ctl->err_flags & kFlagUnsorted)) {
+    // already in line-1 order: the stable order is the identity
+    if (LAST)
+      for (int64_t idx = (int64_t)blockIdx.x * kSortTile + tid;
+           idx < min(p.n, (int64_t)(blockIdx.x + 1) * kSortTile); idx += kSortThreads)
+        p.dst_vals[0][idx] = (uint32_t)idx;
+    return;
+  }
   if (tid == 0) s_tile = (int)atomicAdd(&p.tile_ctr[line], 1u);
   for (int t = tid; t < 8 * kRadix; t += kSortThreads) s_whist[t] = 0;
   __syncthreads();
@@ -180,8 +220,11 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   for (int j = 0; j < kSortIPT; ++j) {
     const int64_t idx = base + (int64_t)warp * 32 * kSortIPT + j * 32 + lane;
     if (idx < p.n) {
-      if (FIRST) {
-        key[j] = SLG ? line_key(pcp[idx], line, p.b) : kin[idx];
+      if (FIRST && SLG && line > 0) {  // derived line: the previous line's order, one field
+        val[j] = p.src_vals[line][idx];
+        key[j] = pass_key(pcp[val[j]], line, p.b);
+      } else if (FIRST) {
+        key[j] = SLG ? pcp[idx] : kin[idx];
         val[j] = (uint32_t)idx;
       } else {
         key[j] = kin[idx];
@@ -194,7 +237,8 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   }
   // warp multisplit: stable rank of each key among equal digits of its warp
   uint32_t* wh = s_whist + warp * kRadix;
-  const int kwidth = SLG ? 3 * p.b : (int)(sizeof(K) * 8);  // bits above are 0 in every key
+  // bits above are 0 in every key
+  const int kwidth = SLG ? (line == 0 ? 3 * p.b : p.b) : (int)(sizeof(K) * 8);
   const int dbits = min(8, max(0, kwidth - shift));
 #pragma unroll
   for (int j = 0; j < kSortIPT; ++j) {
@@ -236,7 +280,7 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   }
   STLOG(1);
   // this digit's count over the whole pass (its latency hides in the look-back)
-  const uint32_t hcount = p.hist[(line * p.passes + p.pass) * kRadix + d];
+  const uint32_t hcount = p.hist[(line * kMaxPasses + p.pass) * kRadix + d];
   // decoupled look-back over preceding tiles of this line
   unsigned long long* st = p.status + ((int64_t)line * p.tiles) * kRadix;
   const unsigned long long ep = (unsigned long long)p.epoch << 34;
@@ -757,56 +801,68 @@ static int launch_pass(fgbd_ctx* ctx, SortPass& p, int nlines) {
   return FGBD_OK;
 }
 
-// Run `passes` onesweep passes over nlines lines.  On return ctx->perm[l]
-// points at the final permutation of line l.
+// SLG (nlines = 3): line 1 takes `passes` passes over its code, then lines 2
+// and 3 ceil(b/8) passes each over one field of the previous line's order.
+// Otherwise: `passes` passes over keys_in (one line).  On return
+// ctx->perm[l] points at the final permutation of line l.
 template <typename K, bool SLG>
 static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
                     const K* keys_in) {
   SortScratch& S = ctx->sort;
   const int tiles = (int)((n + kSortTile - 1) / kSortTile);
-  const int nh = nlines * passes * kRadix;
+  const int passes12 = SLG ? (b + 7) / 8 : 0;
+  const int nh = nlines * kMaxPasses * kRadix;
   FGBD_CUDA(ctx, cudaMemsetAsync(S.hist, 0, nh * sizeof(uint32_t), ctx->stream));
   FGBD_CUDA(ctx, cudaMemsetAsync(S.tile_ctr, 0, kMaxPasses * 3 * sizeof(unsigned), ctx->stream));
   {
     const size_t smem = nh * sizeof(uint32_t);
     const int grid = grid_for(n, ctx->num_sms * ctx->prep_mult);
     if (SLG) {
-      k_prep<K, true><<<grid, kBlock, smem, ctx->stream>>>(
-          ctx->cur_coords, nullptr, n, b, nlines, passes, (K*)ctx->pc, S.hist, ctx->ctl);
+      k_prep<K, true><<<grid, kBlock, smem, ctx->stream>>>(ctx->cur_coords, nullptr, n, b, nlines,
+                                                           passes, passes12, (K*)ctx->pc, S.hist,
+                                                           ctx->ctl);
     } else {
-      k_prep<K, false><<<grid, kBlock, smem, ctx->stream>>>(
-          nullptr, keys_in, n, b, nlines, passes, nullptr, S.hist, ctx->ctl);
+      k_prep<K, false><<<grid, kBlock, smem, ctx->stream>>>(nullptr, keys_in, n, b, nlines, passes,
+                                                            0, nullptr, S.hist, ctx->ctl);
     }
     FGBD_LAUNCH(ctx);
   }
-  for (int pass = 0; pass < passes; ++pass) {
-    SortPass p{};
-    for (int l = 0; l < nlines; ++l) {
-      p.src_keys[l] = pass == 0 ? (const void*)keys_in : S.keys[(pass - 1) & 1][l];
-      p.src_vals[l] = pass == 0 ? nullptr : S.vals[(pass - 1) & 1][l];
-      p.dst_keys[l] = S.keys[pass & 1][l];
-      p.dst_vals[l] = S.vals[pass & 1][l];
+  // SLG: one line per launch (each derived line needs the previous order);
+  // stand-alone argsort: its single line
+  for (int line = 0; line < nlines; ++line) {
+    const int lp = (SLG && line > 0) ? passes12 : passes;
+    for (int pass = 0; pass < lp; ++pass) {
+      SortPass p{};
+      for (int l = 0; l < 3; ++l) {
+        p.src_keys[l] = pass == 0 ? (const void*)keys_in : S.keys[(pass - 1) & 1][l];
+        p.src_vals[l] = pass == 0 ? nullptr : S.vals[(pass - 1) & 1][l];
+        p.dst_keys[l] = S.keys[pass & 1][l];
+        p.dst_vals[l] = S.vals[pass & 1][l];
+      }
+      if (SLG && line > 0 && pass == 0) p.src_vals[line] = ctx->perm[line - 1];
+      p.pc = ctx->pc;
+      p.hist = S.hist;
+      p.status = S.status;
+      p.tile_ctr = S.tile_ctr + pass * 3;
+      p.ctl = ctx->ctl;
+      p.n = n;
+      p.b = b;
+      p.pass = pass;
+      p.passes = lp;
+      p.tiles = tiles;
+      p.line0 = line;
+      p.epoch = (++S.epoch) & 0x3fffffffu;
+      if (p.epoch == 0) p.epoch = S.epoch = 1;
+      const bool first = pass == 0, last = pass == lp - 1;
+      int rc;
+      if (first && last) rc = launch_pass<K, true, true, SLG>(ctx, p, 1);
+      else if (first) rc = launch_pass<K, true, false, SLG>(ctx, p, 1);
+      else if (last) rc = launch_pass<K, false, true, SLG>(ctx, p, 1);
+      else rc = launch_pass<K, false, false, SLG>(ctx, p, 1);
+      if (rc) return rc;
     }
-    p.pc = ctx->pc;
-    p.hist = S.hist;
-    p.status = S.status;
-    p.tile_ctr = S.tile_ctr + pass * 3;
-    p.n = n;
-    p.b = b;
-    p.pass = pass;
-    p.passes = passes;
-    p.tiles = tiles;
-    p.epoch = (++S.epoch) & 0x3fffffffu;
-    if (p.epoch == 0) p.epoch = S.epoch = 1;
-    const bool first = pass == 0, last = pass == passes - 1;
-    int rc;
-    if (first && last) rc = launch_pass<K, true, true, SLG>(ctx, p, nlines);
-    else if (first) rc = launch_pass<K, true, false, SLG>(ctx, p, nlines);
-    else if (last) rc = launch_pass<K, false, true, SLG>(ctx, p, nlines);
-    else rc = launch_pass<K, false, false, SLG>(ctx, p, nlines);
-    if (rc) return rc;
+    ctx->perm[line] = S.vals[(lp - 1) & 1][line];
   }
-  for (int l = 0; l < nlines; ++l) ctx->perm[l] = S.vals[(passes - 1) & 1][l];
   return FGBD_OK;
 }
 

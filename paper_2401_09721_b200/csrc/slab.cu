@@ -632,6 +632,7 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
   const bool timing = !(flags & FGBD_FLAG_NO_TIMING);
   cudaEvent_t* ev = parent->ev;
   std::lock_guard<std::mutex> lock(slab_device_mutex(parent->device));
+  NvtxRange nv_frame("fgbd.denoise_slab");
   if (timing) FGBD_CUDA(parent, cudaEventRecord(ev[0], parent->stream));
   // ---- phase 1: upload own points, sort, block lists, own Y ------------------
   int64_t off = 0;
