@@ -37,7 +37,10 @@ constexpr int kRedGrid = 148 * 4;      // fixed partition => deterministic sums
 constexpr int kRowsGrid = 148 * 8;     // k_rows partition (fixed => deterministic sigma_g)
 constexpr int kNeGrid = 148 * 16;      // NE blocks (96 threads: one warp per channel)
 constexpr int kSortThreads = 256;
-constexpr int kSortIPT = 16;
+#ifndef FGBD_SORT_IPT
+#define FGBD_SORT_IPT 16
+#endif
+constexpr int kSortIPT = FGBD_SORT_IPT;
 constexpr int kSortTile = kSortThreads * kSortIPT;  // keys per onesweep tile
 constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;
@@ -169,6 +172,7 @@ struct fgbd_ctx {
   int64_t l2_bytes = 0;         // device L2 capacity
   int reorder_rows = 1;         // FGBD_REORDER: denoise-path rows in scan-line-1 order
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
+  int sort_derived = 1;         // FGBD_SORT_DERIVED: lines 2/3 by one field of the previous order
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)
   fgbd::Ctl* ctl = nullptr;     // device

@@ -65,8 +65,9 @@ constexpr int kFlagUnsorted = 16;  // Ctl::err_flags: input is not in scan-line-
 // sort key of line l's pass p: line 0 its code; lines 1 / 2 (derived) the
 // x / y field of the line-1 code
 template <typename K>
-__device__ __forceinline__ K pass_key(K code, int line, int b) {
+__device__ __forceinline__ K pass_key(K code, int line, int b, bool derived) {
   if (line == 0) return code;
+  if (!derived) return line_key(code, line, b);
   const K m = (K(1) << b) - 1;
   return line == 1 ? (code & m) : ((code >> b) & m);
 }
@@ -77,7 +78,8 @@ template <typename K, bool FROM_COORDS>
 __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coords,
                                                  const K* __restrict__ keys_in, int64_t n,
                                                  int b, int nlines, int passes0, int passes12,
-                                                 K* __restrict__ pc, uint32_t* __restrict__ hist,
+                                                 int derived, K* __restrict__ pc,
+                                                 uint32_t* __restrict__ hist,
                                                  Ctl* __restrict__ ctl) {
   extern __shared__ uint32_t s_hist[];  // [nlines][kMaxPasses][256]
   const int nh = nlines * kMaxPasses * kRadix;
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
     }
     const unsigned vmask = __ballot_sync(kFull, valid);
     for (int l = 0; l < nlines; ++l) {
-      const K key = FROM_COORDS ? pass_key(code, l, b) : code;
+      const K key = FROM_COORDS ? pass_key(code, l, b, derived != 0) : code;
       const int passes = l == 0 ? passes0 : passes12;
       for (int p = 0; p < passes; ++p) {
         const unsigned d = valid ? (unsigned)((key >> (8 * p)) & 0xff) : 0x100u;
@@ -154,6 +156,7 @@ struct SortPass {
   int64_t n;
   int b, pass, passes, tiles;
   int line0;                    // line of blockIdx.y == 0
+  int derived;                  // SLG lines 2/3 sort one field of the previous line's order
   unsigned int epoch;
 };
 
@@ -220,11 +223,11 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   for (int j = 0; j < kSortIPT; ++j) {
     const int64_t idx = base + (int64_t)warp * 32 * kSortIPT + j * 32 + lane;
     if (idx < p.n) {
-      if (FIRST && SLG && line > 0) {  // derived line: the previous line's order, one field
+      if (FIRST && SLG && line > 0 && p.derived) {  // the previous line's order, one field
         val[j] = p.src_vals[line][idx];
-        key[j] = pass_key(pcp[val[j]], line, p.b);
+        key[j] = pass_key(pcp[val[j]], line, p.b, true);
       } else if (FIRST) {
-        key[j] = SLG ? pcp[idx] : kin[idx];
+        key[j] = SLG ? line_key(pcp[idx], line, p.b) : kin[idx];
         val[j] = (uint32_t)idx;
       } else {
         key[j] = kin[idx];
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(kSortThreads, FGBD_SORT_MINB) k_onesweep(SortP
   // warp multisplit: stable rank of each key among equal digits of its warp
   uint32_t* wh = s_whist + warp * kRadix;
   // bits above are 0 in every key
-  const int kwidth = SLG ? (line == 0 ? 3 * p.b : p.b) : (int)(sizeof(K) * 8);
+  const int kwidth = SLG ? ((line == 0 || !p.derived) ? 3 * p.b : p.b) : (int)(sizeof(K) * 8);
   const int dbits = min(8, max(0, kwidth - shift));
 #pragma unroll
   for (int j = 0; j < kSortIPT; ++j) {
@@ -810,7 +813,8 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
                     const K* keys_in) {
   SortScratch& S = ctx->sort;
   const int tiles = (int)((n + kSortTile - 1) / kSortTile);
-  const int passes12 = SLG ? (b + 7) / 8 : 0;
+  const bool derived = SLG && ctx->sort_derived;
+  const int passes12 = SLG ? (derived ? (b + 7) / 8 : passes) : 0;
   const int nh = nlines * kMaxPasses * kRadix;
   FGBD_CUDA(ctx, cudaMemsetAsync(S.hist, 0, nh * sizeof(uint32_t), ctx->stream));
   FGBD_CUDA(ctx, cudaMemsetAsync(S.tile_ctr, 0, kMaxPasses * 3 * sizeof(unsigned), ctx->stream));
@@ -819,18 +823,21 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
     const int grid = grid_for(n, ctx->num_sms * ctx->prep_mult);
     if (SLG) {
       k_prep<K, true><<<grid, kBlock, smem, ctx->stream>>>(ctx->cur_coords, nullptr, n, b, nlines,
-                                                           passes, passes12, (K*)ctx->pc, S.hist,
-                                                           ctx->ctl);
+                                                           passes, passes12, derived ? 1 : 0,
+                                                           (K*)ctx->pc, S.hist, ctx->ctl);
     } else {
       k_prep<K, false><<<grid, kBlock, smem, ctx->stream>>>(nullptr, keys_in, n, b, nlines, passes,
-                                                            0, nullptr, S.hist, ctx->ctl);
+                                                            0, 0, nullptr, S.hist, ctx->ctl);
     }
     FGBD_LAUNCH(ctx);
   }
-  // SLG: one line per launch (each derived line needs the previous order);
-  // stand-alone argsort: its single line
-  for (int line = 0; line < nlines; ++line) {
-    const int lp = (SLG && line > 0) ? passes12 : passes;
+  // derived: one line per launch (each needs the previous line's order);
+  // otherwise every line in each launch (blockIdx.y), line 1 skipping when
+  // the input is already sorted
+  const int groups = derived ? nlines : 1, per_launch = derived ? 1 : nlines;
+  for (int lg = 0; lg < groups; ++lg) {
+    const int line = lg;
+    const int lp = (derived && line > 0) ? passes12 : passes;
     for (int pass = 0; pass < lp; ++pass) {
       SortPass p{};
       for (int l = 0; l < 3; ++l) {
@@ -839,7 +846,7 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
         p.dst_keys[l] = S.keys[pass & 1][l];
         p.dst_vals[l] = S.vals[pass & 1][l];
       }
-      if (SLG && line > 0 && pass == 0) p.src_vals[line] = ctx->perm[line - 1];
+      if (derived && line > 0 && pass == 0) p.src_vals[line] = ctx->perm[line - 1];
       p.pc = ctx->pc;
       p.hist = S.hist;
       p.status = S.status;
@@ -851,17 +858,18 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
       p.passes = lp;
       p.tiles = tiles;
       p.line0 = line;
+      p.derived = derived ? 1 : 0;
       p.epoch = (++S.epoch) & 0x3fffffffu;
       if (p.epoch == 0) p.epoch = S.epoch = 1;
       const bool first = pass == 0, last = pass == lp - 1;
       int rc;
-      if (first && last) rc = launch_pass<K, true, true, SLG>(ctx, p, 1);
-      else if (first) rc = launch_pass<K, true, false, SLG>(ctx, p, 1);
-      else if (last) rc = launch_pass<K, false, true, SLG>(ctx, p, 1);
-      else rc = launch_pass<K, false, false, SLG>(ctx, p, 1);
+      if (first && last) rc = launch_pass<K, true, true, SLG>(ctx, p, per_launch);
+      else if (first) rc = launch_pass<K, true, false, SLG>(ctx, p, per_launch);
+      else if (last) rc = launch_pass<K, false, true, SLG>(ctx, p, per_launch);
+      else rc = launch_pass<K, false, false, SLG>(ctx, p, per_launch);
       if (rc) return rc;
     }
-    ctx->perm[line] = S.vals[(lp - 1) & 1][line];
+    for (int l = line; l < line + per_launch; ++l) ctx->perm[l] = S.vals[(lp - 1) & 1][l];
   }
   return FGBD_OK;
 }
