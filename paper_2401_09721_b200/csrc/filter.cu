@@ -45,6 +45,16 @@
 #ifndef FGBD_LF_PFD
 #define FGBD_LF_PFD 2
 #endif
+#ifndef FGBD_LF_RCPDIV
+#define FGBD_LF_RCPDIV 1  // the step's three quotients via one reciprocal (div_rcp)
+#endif
+#ifndef FGBD_LF_SPLITBAR
+// split-phase grid barrier: arrive right after a step's rows and partials are
+// stored, run the lagged select_q decision, then wait -- the decision no
+// longer sits between the slowest block's sweep and the barrier (1: on;
+// 0: cooperative_groups grid.sync() after the decision)
+#define FGBD_LF_SPLITBAR 0
+#endif
 #ifndef FGBD_LF_ELLSMEM
 // graph slots of the next FGBD_LF_ELLSMEM rows via cp.async into shared memory (0: registers;
 // profiles/r1_summary.md r1c: 1 stage -2.5% filter time, 2 / 3 stages slower -- less L1)
@@ -185,6 +195,7 @@ struct StepArgs {
   int halo;         // TMA-staged sweep: window rows either side of a row tile
   const uint32_t* rowid;  // row -> point when rows are in scan-line-1 order (else null)
   unsigned long long* flags;  // P2P: per-block "step published" words (monotone across launches)
+  unsigned int* gbar;         // split-phase grid barrier: [0] arrivals, [1] generation
   unsigned long long base;    // P2P: this launch's flag base (published value = base + step)
 };
 
@@ -271,6 +282,26 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// out = (d f + acc) / (2 d) per channel (filtering.py:148-155); d = 0 keeps f
+__device__ __forceinline__ double4 finish_row(double d, const double4& f, double acc0,
+                                              double acc1, double acc2) {
+  if (d == 0.0) return f;
+  const double d2 = __dmul_rn(2.0, d);
+#if FGBD_LF_RCPDIV
+  // one reciprocal for the three quotients; div_rcp is the correctly
+  // rounded a / b (device_util.cuh), so the bits are unchanged
+  if (rcp_ok(d2)) {
+    const double y = __drcp_rn(d2);
+    return make_double4(div_rcp(__dadd_rn(__dmul_rn(d, f.x), acc0), d2, y),
+                        div_rcp(__dadd_rn(__dmul_rn(d, f.y), acc1), d2, y),
+                        div_rcp(__dadd_rn(__dmul_rn(d, f.z), acc2), d2, y), 0.0);
+  }
+#endif
+  return make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
+                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
+                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
+}
+
 __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const float (&wf)[kSlots],
                                                   const double4* in, int64_t i, uint64_t pol_keep) {
   const double4 f = ld_row_hint(in + i, pol_keep);
@@ -317,12 +348,7 @@ __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const
     }
   }
 #endif
-  const double d = __dadd_rn(hi, lo);
-  if (d == 0.0) return f;
-  const double d2 = __dmul_rn(2.0, d);
-  return make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
-                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
-                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
+  return finish_row(__dadd_rn(hi, lo), f, acc0, acc1, acc2);
 }
 
 // fp64-weight row for the parity mode (per-step launches only).
@@ -348,12 +374,7 @@ __device__ __forceinline__ double4 row_w64(const StepArgs& a, const double4* in,
       acc2 = __dadd_rn(acc2, __dmul_rn(w[s], g.z));
     }
   }
-  const double d = __dadd_rn(hi, lo);
-  if (d == 0.0) return f;
-  const double d2 = __dmul_rn(2.0, d);
-  return make_double4(__ddiv_rn(__dadd_rn(__dmul_rn(d, f.x), acc0), d2),
-                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.y), acc1), d2),
-                      __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
+  return finish_row(__dadd_rn(hi, lo), f, acc0, acc1, acc2);
 }
 
 // select_q bookkeeping after step q (filtering.py:244-255).  Pure function
@@ -686,6 +707,29 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
+// Split-phase grid barrier over the co-resident blocks of a cooperative
+// launch: the arrive / wait halves of cooperative_groups' grid.sync() (one
+// atomic per block; block 0 adds 2^31 - (blocks - 1), so the word's top bit
+// flips exactly when the last block arrives).
+__device__ __forceinline__ unsigned int grid_arrive(unsigned int* bar) {
+  __syncthreads();  // every thread's stores of this step are issued
+  unsigned int old = 0;
+  if (threadIdx.x == 0) {
+    const unsigned int nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+    __threadfence();
+    old = atomicAdd(bar, nb);
+  }
+  return old;  // meaningful in thread 0
+}
+__device__ __forceinline__ void grid_wait(unsigned int* bar, unsigned int old) {
+  if (threadIdx.x == 0) {
+    while ((((*(volatile unsigned int*)bar) ^ old) & 0x80000000u) == 0) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 template <int WM, bool SELECT, int BLK = kBlock, int MINB = 3, bool TMA = false,
           bool P2P = false>
 __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
@@ -803,6 +847,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       __syncthreads();
       if (threadIdx.x == 0) st_release_u64(a.flags + blockIdx.x, a.base + c + 1);
     }
+    constexpr bool kSplit = FGBD_LF_SPLITBAR && !P2P;
+    unsigned int gen0 = 0;
+    if (kSplit) gen0 = grid_arrive(a.gbar);  // step c+1 is stored: arrive now, wait below
     if (SELECT && !decided) {
       if (P2P) {
         wait_blocks(a.flags, 0, nb - 1, blockIdx.x, a.base + c);
@@ -825,12 +872,17 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       if (threadIdx.x == 0) decide(t);
       __syncthreads();
     }
+    // (a stop is decided identically by every block, and every block has
+    // arrived, so leaving here never strands a waiter)
     if (!SELECT && c >= s_qmax) break;
     if (s_st.stop) break;
     if (P2P) {
       // x_{c+1} of every block this one reads (and that reads this one) is
       // published; the acquire orders this block's next loads after it
       wait_blocks(a.flags, s_dep_lo, s_dep_hi, blockIdx.x, a.base + c + 1);
+    } else if (kSplit) {
+      TLOG(c, 2);
+      grid_wait(a.gbar, gen0);
     } else {
       TLOG(c, 2);
       grid.sync();
@@ -1066,6 +1118,7 @@ static StepArgs step_args(fgbd_ctx* ctx, int64_t n) {
   a.part = ctx->partials;
   a.ctl = ctx->ctl;
   a.rowid = ctx->g_reordered ? ctx->rowid : nullptr;
+  a.gbar = ctx->tickets;
   return a;
 }
 

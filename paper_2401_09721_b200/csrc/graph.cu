@@ -81,8 +81,10 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
                                                  int derived, K* __restrict__ pc,
                                                  uint32_t* __restrict__ hist,
                                                  Ctl* __restrict__ ctl) {
-  extern __shared__ uint32_t s_hist[];  // [nlines][kMaxPasses][256]
-  const int nh = nlines * kMaxPasses * kRadix;
+  // shared histograms packed (line 0's passes, then line 1's, line 2's);
+  // hist (global) keeps the [line][kMaxPasses][256] layout
+  extern __shared__ uint32_t s_hist[];
+  const int nh = (passes0 + (nlines - 1) * passes12) * kRadix;
   for (int t = threadIdx.x; t < nh; t += blockDim.x) s_hist[t] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -116,6 +118,7 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
     for (int l = 0; l < nlines; ++l) {
       const K key = FROM_COORDS ? pass_key(code, l, b, derived != 0) : code;
       const int passes = l == 0 ? passes0 : passes12;
+      uint32_t* sh = s_hist + (l == 0 ? 0 : passes0 + (l - 1) * passes12) * kRadix;
       for (int p = 0; p < passes; ++p) {
         const unsigned d = valid ? (unsigned)((key >> (8 * p)) & 0xff) : 0x100u;
         // a digit shared by the whole warp (raster-ordered input, high
@@ -123,10 +126,9 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
         // contend when equal digits are scattered across the warp
         const unsigned d0 = __shfl_sync(kFull, d, 0);
         if (__all_sync(kFull, d == d0) && d0 < 0x100u) {
-          if (lane == 0)
-            atomicAdd(&s_hist[(l * kMaxPasses + p) * kRadix + d0], (uint32_t)__popc(vmask));
+          if (lane == 0) atomicAdd(&sh[p * kRadix + d0], (uint32_t)__popc(vmask));
         } else if (valid) {
-          atomicAdd(&s_hist[(l * kMaxPasses + p) * kRadix + d], 1u);
+          atomicAdd(&sh[p * kRadix + d], 1u);
         }
       }
     }
@@ -134,8 +136,13 @@ __global__ void __launch_bounds__(kBlock) k_prep(const int64_t* __restrict__ coo
   if (bad) atomicOr(&ctl->err_flags, 1);
   if (__any_sync(kFull, unsorted) && lane == 0) atomicOr(&ctl->err_flags, kFlagUnsorted);
   __syncthreads();
-  for (int t = threadIdx.x; t < nh; t += blockDim.x)
-    if (s_hist[t]) atomicAdd(&hist[t], s_hist[t]);
+  for (int t = threadIdx.x; t < nh; t += blockDim.x) {
+    if (!s_hist[t]) continue;
+    const int slot = t / kRadix;  // packed (line, pass) -> [line][kMaxPasses]
+    const int l = slot < passes0 ? 0 : 1 + (slot - passes0) / max(passes12, 1);
+    const int p = l == 0 ? slot : (slot - passes0) % max(passes12, 1);
+    atomicAdd(&hist[(l * kMaxPasses + p) * kRadix + (t % kRadix)], s_hist[t]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -817,9 +824,10 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
   const int passes12 = SLG ? (derived ? (b + 7) / 8 : passes) : 0;
   const int nh = nlines * kMaxPasses * kRadix;
   FGBD_CUDA(ctx, cudaMemsetAsync(S.hist, 0, nh * sizeof(uint32_t), ctx->stream));
+  const int nh_used = (passes + (nlines - 1) * passes12) * kRadix;
   FGBD_CUDA(ctx, cudaMemsetAsync(S.tile_ctr, 0, kMaxPasses * 3 * sizeof(unsigned), ctx->stream));
   {
-    const size_t smem = nh * sizeof(uint32_t);
+    const size_t smem = nh_used * sizeof(uint32_t);
     const int grid = grid_for(n, ctx->num_sms * ctx->prep_mult);
     if (SLG) {
       k_prep<K, true><<<grid, kBlock, smem, ctx->stream>>>(ctx->cur_coords, nullptr, n, b, nlines,
