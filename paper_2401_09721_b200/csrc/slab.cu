@@ -232,7 +232,16 @@ struct SlabState {
   double best_crit, prev;
 };
 
-__global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Like k_lf_run (csrc/filter.cu): a row's three 16-byte graph loads land by
+// cp.async in this thread's own shared-memory slots one sweep iteration
+// ahead, and the graph row two iterations ahead is prefetched into L2, so
+// the sweep holds no graph registers and runs 3 blocks per SM.
+__global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
+  extern __shared__ __align__(16) int4 s_ell[];  // [2 stages][3 pairs][kBlock]
   __shared__ double s_red[32 * 3];
   __shared__ SlabState s_st;
   __shared__ double s_sy[3], s_sv2;
@@ -283,30 +292,39 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
                                : (int64_t)lb * blockDim.x + threadIdx.x;
       const int64_t end = a.contiguous ? min(n_own, (int64_t)(lb + 1) * chunk) : n_own;
       const int64_t rstep = a.contiguous ? (int64_t)blockDim.x : (int64_t)a.bpg * blockDim.x;
-      int nbn[kSlots];
-      float wn[kSlots];
-      auto load_slots = [&](int64_t row, int (&nb)[kSlots], float (&w)[kSlots]) {
+      const int T = blockDim.x;
+      int stage = 0;
+      auto issue = [&](int64_t row, int st) {
+        if (row < end)
+#pragma unroll
+          for (int s = 0; s < kSlots; s += 2)
+            asm volatile(
+                "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
+                    smem_addr(s_ell + (st * 3 + (s >> 1)) * T + threadIdx.x)),
+                "l"(G.E.nbr + eslot(s, n_own, row)), "l"(pol_stream)
+                : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      issue(i, 0);
+      while (i < end) {
+        const int64_t inext = i + rstep;
+        issue(inext, stage ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        int nb[kSlots];
+        float w[kSlots];
 #pragma unroll
         for (int s = 0; s < kSlots; s += 2) {
-          const int4 pr = ld_pair_hint(
-              reinterpret_cast<const int2*>(G.E.nbr + eslot(s, n_own, row)), pol_stream);
+          const int4 pr = s_ell[(stage * 3 + (s >> 1)) * T + threadIdx.x];
           nb[s] = pr.x;  // GLOBAL row | below-flag (bit 31)
           w[s] = __int_as_float(pr.y);
           nb[s + 1] = pr.z;
           w[s + 1] = __int_as_float(pr.w);
         }
-      };
-      if (i < end) load_slots(i, nbn, wn);
-      while (i < end) {
-        int nb[kSlots];
-        float w[kSlots];
+        stage ^= 1;
+        if (i + 2 * rstep < end)
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s) {
-          nb[s] = nbn[s];
-          w[s] = wn[s];
-        }
-        const int64_t inext = i + rstep;
-        if (inext < end) load_slots(inext, nbn, wn);
+          for (int s = 0; s < kSlots; s += 2)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(G.E.nbr + eslot(s, n_own, i + 2 * rstep)));
         const int64_t gi = lo + i;
         const double4 f = ld_row_hint(own_in + gi, pol_keep);
         double4 gv[kSlots];
@@ -346,6 +364,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_lf_slab(SlabArgs a) {
         }
         i = inext;
       }
+      asm volatile("cp.async.wait_all;" ::: "memory");
     }
     block_sum<3>(sx, s_red);
     double* part = a.part + ((int64_t)g * a.bpg + lb) * 4;
@@ -783,8 +802,10 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
     a.epoch = s->epoch;
     a.select = cached_q < 0;
     a.fixed_steps = cached_q < 0 ? 0 : cached_q;
+    const int smem = 2 * 3 * kBlock * (int)sizeof(int4);
     int per_sm = 0;
-    FGBD_CUDA(parent, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lf_slab, kBlock, 0));
+    FGBD_CUDA(parent,
+              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lf_slab, kBlock, smem));
     const int capacity = std::min(std::max(1, per_sm) * parent->num_sms, s->bpg_cap);
     int64_t max_rows = 1;
     for (int g = 0; g < s->groups; ++g) max_rows = std::max(max_rows, s->loc[g].g.n_own);
@@ -797,7 +818,7 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
               cudaMemsetAsync(s->gbar, 0, 2 * s->groups * sizeof(unsigned), parent->stream));
     void* args[] = {&a};
     FGBD_CUDA(parent, cudaLaunchCooperativeKernel((void*)k_lf_slab, s->groups * a.bpg, kBlock,
-                                                  args, 0, parent->stream));
+                                                  args, smem, parent->stream));
     FGBD_LAUNCH(parent);
   }
   if (timing) FGBD_CUDA(parent, cudaEventRecord(ev[6], parent->stream));
