@@ -373,10 +373,15 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
     group_barrier(gbar, a.bpg, ctl);  // this rank's rows of step q+1 are written
     const int par = (q + 1) & 1;
     const unsigned long long tick = (a.epoch << 32) | (unsigned long long)(q + 1);
-    if (lb == 0 && threadIdx.x == 0) {
-      double t[3] = {0.0, 0.0, 0.0};
-      for (int b = 0; b < a.bpg; ++b)
+    double t[3] = {0.0, 0.0, 0.0};
+    if (lb == 0) {
+      // the rank's total: the leader block reduces its blocks' partials
+      // (strided over its threads, then the fixed block tree; thread 0 holds it)
+      for (int b = threadIdx.x; b < a.bpg; b += blockDim.x)
         for (int k = 0; k < 3; ++k) t[k] += ld_cg(a.part + ((int64_t)g * a.bpg + b) * 4 + k);
+      block_sum<3>(t, s_red);
+    }
+    if (lb == 0 && threadIdx.x == 0) {
       for (int p = 0; p < P; ++p)
         for (int k = 0; k < 3; ++k) a.slots[p][(par * P + r) * 4 + k] = t[k];
       __threadfence_system();
