@@ -455,6 +455,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_LF_HALO")) ctx->lf_halo = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("FGBD_SORT_DERIVED")) ctx->sort_derived = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_HOST_THREADS")) ctx->host_threads = std::max(0, std::atoi(v));
   if (ensure_capacity(ctx, max_points > 0 ? max_points : 1, 0) != FGBD_OK) {
     set_error(nullptr, FGBD_E_CUDA, ctx->err);
     fgbd_ctx_destroy(ctx);
@@ -480,6 +481,7 @@ void fgbd_ctx_destroy(fgbd_ctx* ctx) {
   if (ctx->aux) cudaFree(ctx->aux);
   if (ctx->p2p_flags) cudaFree(ctx->p2p_flags);
   if (ctx->held_coords) cudaFree(ctx->held_coords);
+  destroy_stager(ctx);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->side) cudaStreamSynchronize(ctx->side);
@@ -564,12 +566,18 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   // wait for another context's persistent filter to release the SMs.
   const double* frame_colors = colors;
   bool colors_dev = dev;
-  if (!dev && !trusted && (rc = h2d(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), false)))
+  if (!dev && !trusted &&
+      (rc = host_to_device(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), ctx->stream, 0)))
     return rc;
   if (may_reuse && !dev) {
-    if ((rc = h2d(ctx, ctx->out, colors, 3 * n * sizeof(double), false))) return rc;
+    if ((rc = host_to_device(ctx, ctx->out, colors, 3 * n * sizeof(double), ctx->stream, 1)))
+      return rc;
     frame_colors = ctx->out;
     colors_dev = true;
+  } else if (!dev) {
+    // pageable colours are staged into pinned memory while the coordinates
+    // travel; their DMA then overlaps the graph build
+    frame_colors = static_cast<const double*>(host_prestage(ctx, colors, 3 * n * sizeof(double), 1));
   }
   bool reuse = false;
   if (trusted) {

@@ -28,6 +28,7 @@
 
 namespace fgbd {
 struct EllRef;
+struct HostStager;
 }
 
 namespace fgbd {
@@ -217,6 +218,9 @@ struct fgbd_ctx {
 
   int launches = 0;
   std::string err;
+  // pageable host inputs: parallel staging through pinned memory (hoststage.cu)
+  fgbd::HostStager* stager = nullptr;
+  int host_threads = 6;           // FGBD_HOST_THREADS (0: the driver's own pageable copy)
 };
 
 namespace fgbd {
@@ -246,6 +250,15 @@ struct NvtxRange {
 };
 
 int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64);
+// host -> device from host memory: pageable sources go through the
+// context's pinned staging (region 0 or 1) in parallel chunks, each chunk's
+// DMA issued as soon as it has landed; pinned sources copy directly
+int host_to_device(fgbd_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s,
+                   int region);
+// pageable src -> pinned staging region (blocking, parallel); returns the
+// pointer to copy from (src itself when it is pinned or small)
+const void* host_prestage(fgbd_ctx* ctx, const void* src, size_t bytes, int region);
+void destroy_stager(fgbd_ctx* ctx);
 int require_point_rows(fgbd_ctx* ctx);
 // (N,3) colours (host or device) -> BUF_Y in the (N,4) layout
 int upload_colors(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev);
