@@ -455,6 +455,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_LF_HALO")) ctx->lf_halo = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("FGBD_SORT_DERIVED")) ctx->sort_derived = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_ROWS_GRID")) ctx->rows_grid = std::atoi(v);
   if (const char* v = std::getenv("FGBD_HOST_THREADS")) ctx->host_threads = std::max(0, std::atoi(v));
   if (ensure_capacity(ctx, max_points > 0 ? max_points : 1, 0) != FGBD_OK) {
     set_error(nullptr, FGBD_E_CUDA, ctx->err);

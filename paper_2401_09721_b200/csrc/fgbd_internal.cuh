@@ -35,7 +35,7 @@ namespace fgbd {
 
 constexpr int kBlock = 256;
 constexpr int kRedGrid = 148 * 4;      // fixed partition => deterministic sums
-constexpr int kRowsGrid = 148 * 8;     // k_rows partition (fixed => deterministic sigma_g)
+constexpr int kRowsGrid = 148 * 8;     // k_rows grid cap (sigma_g is exact: any grid gives its bits)
 constexpr int kNeGrid = 148 * 16;      // NE blocks (96 threads: one warp per channel)
 constexpr int kSortThreads = 256;
 #ifndef FGBD_SORT_IPT
@@ -174,6 +174,7 @@ struct fgbd_ctx {
   int reorder_rows = 1;         // FGBD_REORDER: denoise-path rows in scan-line-1 order
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
   int sort_derived = 1;         // FGBD_SORT_DERIVED: lines 2/3 by one field of the previous order
+  int rows_grid = 0;            // FGBD_ROWS_GRID: k_rows grid, 0 = 8 blocks/SM (grid-stride), 1 = one row per thread
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)
   fgbd::Ctl* ctl = nullptr;     // device

@@ -897,7 +897,7 @@ static int graph_impl(fgbd_ctx* ctx, int64_t n, int b, bool reorder) {
                                                   ctx->cand, pos, ctx->ctl);
     FGBD_LAUNCH(ctx);
   }
-  const int grid = grid_for(n, kRowsGrid);
+  const int grid = grid_for(n, ctx->rows_grid == 1 ? (1 << 30) : kRowsGrid);
   if (b > 15) {
     k_rows<K, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b, pos, ctx->rowid,
                                                       EllRef{ctx->nbr, ctx->pay}, ctx->meta, ctx->partials,
@@ -1334,7 +1334,7 @@ static int slab_rows_impl(fgbd_ctx* ctx, SlabGC& g) {
   const int rgrid = grid_for(1 + 2 * g.blk_cap, ctx->num_sms * 8);
   k_resolve<K><<<rgrid, kBlock, 0, ctx->stream>>>(g, ctx->cand);
   FGBD_LAUNCH(ctx);
-  const int grid = grid_for(n, kRowsGrid);
+  const int grid = grid_for(n, ctx->rows_grid == 1 ? (1 << 30) : kRowsGrid);
   k_rows<K, false, true><<<grid, kBlock, 0, ctx->stream>>>(
       ctx->cand, (const K*)g.ext_pc, n, g.b, g.ext_pos, ctx->rowid, EllRef{ctx->nbr, ctx->pay},
       ctx->meta, ctx->partials, ctx->ctl, RowsSlab{g.ext_gidx, g.lo});
