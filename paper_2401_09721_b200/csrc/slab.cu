@@ -195,31 +195,6 @@ struct SlabArgs {
   int contiguous;            // rows per block: contiguous range (1) or grid-stride waves (0)
 };
 
-// Barrier over the bpg co-resident blocks of one group (sense-reversing).
-__device__ __forceinline__ void group_barrier(unsigned int* bar, int nblocks, Ctl* ctl) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int* gen = bar + 1;
-    const unsigned int g0 = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == (unsigned)nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      const long long t0 = clock64();
-      while (*gen == g0) {
-        if (clock64() - t0 > (1ll << 35)) {  // ~17 s: never hang the GPU; report it
-          atomicOr(&ctl->err_flags, 4);
-          break;
-        }
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 __device__ __forceinline__ int owner_of(const SlabArgs& a, int64_t j) {
   int r = 0;
 #pragma unroll 1
@@ -247,6 +222,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
   __shared__ double s_sy[3], s_sv2;
   __shared__ long long s_inc;
   __shared__ int s_qmax, s_mode, s_early, s_mask_all;
+  __shared__ bool s_last;
+  __shared__ unsigned int s_gen;
   const int g = blockIdx.x / a.bpg, lb = blockIdx.x % a.bpg;
   const int r = a.rank0 + g;
   const int P = a.world;
@@ -270,7 +247,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
     }
   }
   __syncthreads();
-  const int64_t lo = a.lo[r], hi = a.lo[r + 1], n_own = G.n_own;
+  const int64_t lo = a.lo[r], n_own = G.n_own;
   const int64_t chunk = ((n_own + a.bpg - 1) / a.bpg + blockDim.x - 1) / blockDim.x * blockDim.x;
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
   unsigned int* gbar = a.gbar + 2 * g;
@@ -332,8 +309,9 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
         for (int s = 0; s < kSlots; ++s) {
           const int64_t j = ell_j(nb[s]);
           FGBD_DCHECK(j >= 0 && j < a.lo[P]);
-          const double4* src =
-              (j >= lo && j < hi) ? own_in : a.bufs[owner_of(a, j)][ib];  // halo: peer memory
+          const double4* src = own_in;
+          if (__builtin_expect((uint64_t)(j - lo) >= (uint64_t)n_own, 0))
+            src = a.bufs[owner_of(a, j)][ib];  // halo: the owner's buffer (peer memory)
           gv[s] = ld_row_hint(src + j, pol_keep);
         }
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, dlo = 0.0, dhi = 0.0;
@@ -370,32 +348,54 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
     double* part = a.part + ((int64_t)g * a.bpg + lb) * 4;
     if (threadIdx.x == 0)
       for (int k = 0; k < 3; ++k) part[k] = sx[k];
-    group_barrier(gbar, a.bpg, ctl);  // this rank's rows of step q+1 are written
+    // Arrive.  The group's LAST block to arrive reduces the rank's partials
+    // (strided over its threads, then the fixed block tree), stores the total
+    // into every rank's slot, publishes the step tick, waits for every
+    // rank's tick and releases the group: one group-wide sync per step.
     const int par = (q + 1) & 1;
     const unsigned long long tick = (a.epoch << 32) | (unsigned long long)(q + 1);
-    double t[3] = {0.0, 0.0, 0.0};
-    if (lb == 0) {
-      // the rank's total: the leader block reduces its blocks' partials
-      // (strided over its threads, then the fixed block tree; thread 0 holds it)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int gen0 = *(volatile unsigned int*)(gbar + 1);
+      __threadfence();
+      s_last = atomicAdd(gbar, 1u) == (unsigned)a.bpg - 1;
+      s_gen = gen0;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      double t[3] = {0.0, 0.0, 0.0};
       for (int b = threadIdx.x; b < a.bpg; b += blockDim.x)
         for (int k = 0; k < 3; ++k) t[k] += ld_cg(a.part + ((int64_t)g * a.bpg + b) * 4 + k);
       block_sum<3>(t, s_red);
-    }
-    if (lb == 0 && threadIdx.x == 0) {
-      for (int p = 0; p < P; ++p)
-        for (int k = 0; k < 3; ++k) a.slots[p][(par * P + r) * 4 + k] = t[k];
-      __threadfence_system();
-      for (int p = 0; p < P; ++p) st_release_sys(a.flags[p] + r, tick);
-      const long long t0 = clock64();
-      for (int p = 0; p < P; ++p)
-        while (ld_acquire_sys(a.flags[r] + p) < tick) {
-          if (clock64() - t0 > (1ll << 35)) {  // a peer died: report, do not hang
-            atomicOr(&ctl->err_flags, 4);
-            break;
+      if (threadIdx.x == 0) {
+        for (int p = 0; p < P; ++p)
+          for (int k = 0; k < 3; ++k) a.slots[p][(par * P + r) * 4 + k] = t[k];
+        __threadfence_system();
+        for (int p = 0; p < P; ++p) st_release_sys(a.flags[p] + r, tick);
+        const long long t0 = clock64();
+        for (int p = 0; p < P; ++p)
+          while (ld_acquire_sys(a.flags[r] + p) < tick) {
+            if (clock64() - t0 > (1ll << 35)) {  // a peer died: report, do not hang
+              atomicOr(&ctl->err_flags, 4);
+              break;
+            }
           }
+        atomicExch(gbar, 0u);  // every block of the group has arrived
+        __threadfence();
+        atomicAdd(gbar + 1, 1u);  // release
+      }
+    } else if (threadIdx.x == 0) {
+      const long long t0 = clock64();
+      while (*(volatile unsigned int*)(gbar + 1) == s_gen) {
+        if (clock64() - t0 > (1ll << 35)) {  // ~17 s: never hang the GPU; report it
+          atomicOr(&ctl->err_flags, 4);
+          break;
         }
+      }
+      __threadfence();
     }
-    group_barrier(gbar, a.bpg, ctl);  // every rank's rows and totals of step q+1 are visible
+    __syncthreads();  // every rank's rows and totals of step q+1 are visible
     if (threadIdx.x == 0) {
       if (a.select) {
         double tot[3] = {0.0, 0.0, 0.0};
