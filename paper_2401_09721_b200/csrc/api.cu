@@ -456,6 +456,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("FGBD_SORT_DERIVED")) ctx->sort_derived = std::atoi(v);
   if (const char* v = std::getenv("FGBD_ROWS_GRID")) ctx->rows_grid = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_MASK_FOLD")) ctx->mask_fold = std::atoi(v);
   if (const char* v = std::getenv("FGBD_HOST_THREADS")) ctx->host_threads = std::max(0, std::atoi(v));
   if (ensure_capacity(ctx, max_points > 0 ? max_points : 1, 0) != FGBD_OK) {
     set_error(nullptr, FGBD_E_CUDA, ctx->err);
@@ -645,11 +646,18 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = finish_noise(ctx, D, cfg->tau_divisor, &nz))) return rc;
     const double sig = nz.sigma_est;
     const int active = cfg->fslr_enabled && !(sig < cfg->fslr_sigma_floor);
-    if ((rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode, cfg->early_exit,
-                          nullptr)))
+    const bool fold = mask_foldable(ctx, cfg->q_max, w64);
+    if (!fold && (rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode,
+                                   cfg->early_exit, nullptr)))
       return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
-    if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) return rc;
+    if (fold) {
+      if ((rc = launch_select_steps_folded(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode,
+                                           cfg->early_exit)))
+        return rc;
+    } else if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) {
+      return rc;
+    }
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
     if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   }

@@ -174,6 +174,7 @@ struct fgbd_ctx {
   int reorder_rows = 1;         // FGBD_REORDER: denoise-path rows in scan-line-1 order
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
   int sort_derived = 1;         // FGBD_SORT_DERIVED: lines 2/3 by one field of the previous order
+  int mask_fold = 1;            // FGBD_MASK_FOLD: the FSLR mask built by the first filter step
   int rows_grid = 0;            // FGBD_ROWS_GRID: k_rows grid, 0 = 8 blocks/SM (grid-stride), 1 = one row per thread
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)
@@ -316,6 +317,10 @@ int launch_mask(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_ma
 int launch_mask_slab(fgbd_ctx* ctx, int64_t n_own, const double4* y, double sigma_est,
                      int active);
 int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64);
+// the FSLR mask (k_mask) folded into the first filter step
+bool mask_foldable(const fgbd_ctx* ctx, int q_max, int w64);
+int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_max,
+                               int mode, int early_exit);
 // persistent filter: contiguous row range per block (true) or grid-stride waves
 bool lf_contiguous(const fgbd_ctx* ctx, int64_t rows);
 int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf);

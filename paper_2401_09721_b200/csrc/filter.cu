@@ -197,6 +197,15 @@ struct StepArgs {
   unsigned long long* flags;  // P2P: per-block "step published" words (monotone across launches)
   unsigned int* gbar;         // split-phase grid barrier: [0] arrivals, [1] generation
   unsigned long long base;    // P2P: this launch's flag base (published value = base + step)
+  // FSLR mask folded into step 1 (fold != 0, select_q from denoise): step 1
+  // thresholds fslr[] into the mask and sums the select_q initial totals
+  int fold;
+  const double* fslr;
+  double thr;     // 2 sigma_est
+  int active;     // FSLR on (filtering.py:285-295)
+  double* xpart;  // [10][grid]: count, sum_inc y^2 [3], sum_all y^2 [3], sum_all x1^2 [3]
+  int q_max, mode, early_exit;
+  double sv2;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -303,8 +312,10 @@ __device__ __forceinline__ double4 finish_row(double d, const double4& f, double
 }
 
 __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const float (&wf)[kSlots],
-                                                  const double4* in, int64_t i, uint64_t pol_keep) {
+                                                  const double4* in, int64_t i, uint64_t pol_keep,
+                                                  double4* f_out = nullptr) {
   const double4 f = ld_row_hint(in + i, pol_keep);
+  if (f_out) *f_out = f;
   double4 g[kSlots];
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, lo = 0.0, hi = 0.0;
 #if FGBD_LF_DENSE
@@ -417,10 +428,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // FGBD_LF_ELLSMEM by cp.async into this thread's shared-memory slots, which
 // frees 12 registers), and the graph row FGBD_LF_PFD iterations ahead is
 // prefetched into L2.
-template <int WM, bool SUMS>
+template <int WM, bool SUMS, bool FOLD = false>
 __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, double4* out,
                                       bool mask_all, float neg_inv_sg2, double (&sx)[3],
-                                      int4* s_ell) {
+                                      int4* s_ell, double* xs = nullptr /*[10] with FOLD*/) {
   const int64_t n = a.n;
   // rows of this block: a contiguous range walked in blockDim strides (the
   // neighbours of raster / scan-ordered clouds then mostly hit this SM's L1),
@@ -491,9 +502,31 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
 #pragma unroll
       for (int s = 0; s < kSlots; s += 2)
         prefetch_l2(a.E.nbr + eslot(s, n, i + FGBD_LF_PFD * stride));
-    const double4 o = row_from_slots(nbc, wc, in, i, pol_keep);
+    double4 f;
+    const double4 o = row_from_slots(nbc, wc, in, i, pol_keep, FOLD ? &f : nullptr);
     st_row_hint(out + i, o, pol_keep);
-    if (SUMS && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
+    if (FOLD) {
+      // k_mask's work for this row (filtering.py:175-194, 237-243): the
+      // FSLR bit, and the initial totals over included / all rows
+      const bool inc = !(a.active && a.fslr[i] > a.thr);
+      const unsigned bits = __ballot_sync(__activemask(), inc);
+      if ((threadIdx.x & 31) == 0) const_cast<uint32_t*>(a.mask)[i >> 5] = bits;
+      const double y2[3] = {f.x * f.x, f.y * f.y, f.z * f.z};
+      xs[0] += inc ? 1.0 : 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (inc) xs[1 + c] += y2[c];
+        xs[4 + c] += y2[c];
+      }
+      xs[7] = fma(o.x, o.x, xs[7]);
+      xs[8] = fma(o.y, o.y, xs[8]);
+      xs[9] = fma(o.z, o.z, xs[9]);
+      if (inc) {
+        sx[0] = fma(o.x, o.x, sx[0]);
+        sx[1] = fma(o.y, o.y, sx[1]);
+        sx[2] = fma(o.z, o.z, sx[2]);
+      }
+    } else if (SUMS && (mask_all || ((a.mask[i >> 5] >> (i & 31)) & 1u))) {
       sx[0] = fma(o.x, o.x, sx[0]);
       sx[1] = fma(o.y, o.y, sx[1]);
       sx[2] = fma(o.z, o.z, sx[2]);
@@ -707,6 +740,27 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
+// sum of out^2 over the rows this block sweeps (the all-excluded fallback
+// of the folded mask, filtering.py:289-293)
+__device__ __forceinline__ void rows_sumsq(const StepArgs& a, const double4* x, double (&u)[3]) {
+  int64_t i, end, stride;
+  if (a.chunk > 0) {
+    i = (int64_t)blockIdx.x * a.chunk + threadIdx.x;
+    end = min(a.n, (int64_t)(blockIdx.x + 1) * a.chunk);
+    stride = blockDim.x;
+  } else {
+    i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    end = a.n;
+    stride = (int64_t)gridDim.x * blockDim.x;
+  }
+  for (; i < end; i += stride) {
+    const double4 o = ld_row(x + i);
+    u[0] = fma(o.x, o.x, u[0]);
+    u[1] = fma(o.y, o.y, u[1]);
+    u[2] = fma(o.z, o.z, u[2]);
+  }
+}
+
 // Split-phase grid barrier over the co-resident blocks of a cooperative
 // launch: the arrive / wait halves of cooperative_groups' grid.sync() (one
 // atomic per block; block 0 adds 2^31 - (blocks - 1), so the word's top bit
@@ -748,6 +802,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   __shared__ long long s_inc;
   __shared__ int s_qmax, s_mode, s_early, s_mask_all;
   __shared__ int s_dep_lo, s_dep_hi;
+  __shared__ double s_red10[32 * 10];
+  __shared__ int s_fold_stop;
   // step c's block partials land here by bulk copy while step c+1 sweeps
   constexpr bool kBulkPart = SELECT && !P2P;
   __shared__ __align__(16) double s_part[kBulkPart ? 3 * kMaxCoopBlocks + 2 : 2];
@@ -779,7 +835,15 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     }
   }
   if (threadIdx.x == 0) {
-    if (SELECT) {
+    if (SELECT && a.fold) {
+      // the mask and the initial totals come out of step 1 (decided at c = 1)
+      s_st = SelState{0, 0, 0, a.q_max <= 0, BUF_Y, BUF_A, BUF_Y, 0.0, 0.0};
+      s_sv2 = a.sv2;
+      s_qmax = a.q_max;
+      s_mode = a.mode;
+      s_early = a.early_exit;
+      s_mask_all = 0;
+    } else if (SELECT) {
       s_st = SelState{ctl->q, ctl->best_q, ctl->streak, ctl->stop, ctl->in_buf, ctl->out_buf,
                       ctl->best_buf, ctl->best_crit, ctl->prev_crit};
       for (int k = 0; k < 3; ++k) s_sy[k] = ctl->sy[k];
@@ -796,7 +860,6 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     }
   }
   __syncthreads();
-  const bool mask_all = s_mask_all != 0;
   float neg_inv_sg2 = 0.0f;
   if (WM != W_STORED) {
     const double sg = ctl->sigma_g;
@@ -826,10 +889,20 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     TLOG(c, 0);
     if (c < s_qmax) {
       double sx[3] = {0.0, 0.0, 0.0};
-      if (TMA)
+      const bool mask_all = s_mask_all != 0;
+      if (TMA) {
         sweep_tma<SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, tma, sx);
-      else
+      } else if (SELECT && !P2P && a.fold && c == 0) {
+        // step 1 also does k_mask's work (FSLR bits + the initial totals)
+        double xs[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        sweep<WM, SELECT, true>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx,
+                                s_ell, xs);
+        block_sum<10>(xs, s_red10);
+        if (threadIdx.x == 0)
+          for (int k = 0; k < 10; ++k) a.xpart[k * nb + blockIdx.x] = xs[k];
+      } else {
         sweep<WM, SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx, s_ell);
+      }
 #if FGBD_LF_TLOG
       if ((threadIdx.x & 31) == 0 && c < kTlogSteps && (threadIdx.x >> 5) < 16)
         g_wlog[c][blockIdx.x][threadIdx.x >> 5] = gtimer();
@@ -869,7 +942,58 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
           for (int k = 0; k < 3; ++k) t[k] += __ldcg(&part[k * nb + b]);
       }
       block_sum<3>(t, s_red);
-      if (threadIdx.x == 0) decide(t);
+      if (SELECT && !P2P && a.fold && c == 1) {
+        // the FSLR outcome and select_q's initial state (filtering.py:237-243,
+        // 289-293) from step 1's totals -- what k_mask's last block does
+        double x[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+          for (int k = 0; k < 10; ++k) x[k] += __ldcg(&a.xpart[k * nb + b]);
+        block_sum<10>(x, s_red10);
+        if (threadIdx.x == 0) {
+          long long cnt = (long long)x[0];
+          const bool all_ex = (cnt == 0) && a.active;
+          if (all_ex) cnt = a.n;
+          for (int k = 0; k < 3; ++k) s_sy[k] = all_ex ? x[4 + k] : x[1 + k];
+          s_inc = cnt;
+          s_mask_all = all_ex;
+          const double crit0 = cnt > 0 ? criterion(s_sy, s_sy, cnt, s_sv2, s_mode) : 0.0;
+          s_st.best_crit = crit0;
+          s_st.prev = crit0;
+          s_fold_stop = (crit0 == 0.0) || (cnt < 1);
+          if (all_ex)
+            for (int k = 0; k < 3; ++k) t[k] = x[7 + k];  // step 1 over every row
+          if (blockIdx.x == 0) {
+            ctl->trace[0] = crit0;
+            ctl->included = cnt;
+            ctl->all_excluded = all_ex;
+            ctl->mask_all = all_ex;
+            for (int k = 0; k < 3; ++k) ctl->sy[k] = s_sy[k];
+            ctl->sv2 = s_sv2;
+          }
+        }
+        __syncthreads();
+        if (s_mask_all && c < s_qmax) {
+          // step 2 was summed under the (all-zero) mask: sum it over every row
+          double u[3] = {0.0, 0.0, 0.0};
+          rows_sumsq(a, pick_buf(a, ob), u);
+          block_sum<3>(u, s_red);
+          if (threadIdx.x == 0)
+            for (int k = 0; k < 3; ++k)
+              a.part[((c + 1) & (kRing - 1)) * (kBulkPart ? pstride : 3 * nb) + k * nb + blockIdx.x] =
+                  u[k];
+        }
+        if (threadIdx.x == 0) {
+          if (s_fold_stop) {  // the reference runs no step (filtering.py:243)
+            s_st.q = 0;
+            s_st.stop = 1;
+          } else {
+            decide(t);
+          }
+        }
+      } else if (threadIdx.x == 0) {
+        decide(t);
+      }
       __syncthreads();
     }
     // (a stop is decided identically by every block, and every block has
@@ -1213,6 +1337,26 @@ int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64) {
     return FGBD_OK;
   }
   return launch_run_any<true>(ctx, a);
+}
+
+// select_q with k_mask folded into step 1 (default filter kernel only)
+bool mask_foldable(const fgbd_ctx* ctx, int q_max, int w64) {
+  return ctx->mask_fold && ctx->lf_variant == 10 && !w64 && q_max >= 1;
+}
+
+int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_max,
+                               int mode, int early_exit) {
+  StepArgs a = step_args(ctx, n);
+  a.fold = 1;
+  a.fslr = ctx->fslr;
+  a.thr = 2.0 * sigma_est;
+  a.active = active;
+  a.xpart = ctx->partials + (1 << 18);  // 10 x grid, clear of the step partials
+  a.q_max = q_max;
+  a.mode = mode;
+  a.early_exit = early_exit;
+  a.sv2 = sigma_est * sigma_est;
+  return launch_run<W_STORED, true>(ctx, a);
 }
 
 int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf) {
