@@ -622,6 +622,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
 
   fgbd_noise nz;
   std::memset(&nz, 0, sizeof(nz));
+  bool folded = false;  // NE finished on the device + the mask folded into the filter
   if (cached_q >= 0) {
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
     int fin = BUF_Y;
@@ -636,6 +637,22 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
       ctx->g_have_weights = 1;
       ctx->g_weights64 = 0;
     }
+    folded = mask_foldable(ctx, cfg->q_max, w64);
+  }
+  if (cached_q < 0 && folded) {
+    // the whole frame without a host round trip: NE finished on the device
+    // (bit-identical to finish_noise), the FSLR mask built by step 1
+    if ((rc = launch_finish_noise(ctx, cfg->patch_size, cfg->tau_divisor, cfg->fslr_enabled,
+                                  cfg->fslr_sigma_floor)))
+      return rc;
+    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
+    if ((rc = launch_select_steps_folded(ctx, n, cfg->q_max, cfg->criterion_mode,
+                                         cfg->early_exit)))
+      return rc;
+    if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
+    if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
+  } else if (cached_q < 0) {
+    const int D = cfg->patch_size;
     if ((rc = pull_ctl(ctx))) return rc;
     if ((rc = check_graph_ctl(ctx, bits))) return rc;
     const int maxdeg = ctx->ctl_host->max_deg;
@@ -646,31 +663,27 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = finish_noise(ctx, D, cfg->tau_divisor, &nz))) return rc;
     const double sig = nz.sigma_est;
     const int active = cfg->fslr_enabled && !(sig < cfg->fslr_sigma_floor);
-    const bool fold = mask_foldable(ctx, cfg->q_max, w64);
-    if (!fold && (rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode,
-                                   cfg->early_exit, nullptr)))
+    if ((rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode, cfg->early_exit,
+                          nullptr)))
       return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
-    if (fold) {
-      if ((rc = launch_select_steps_folded(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode,
-                                           cfg->early_exit)))
-        return rc;
-    } else if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) {
-      return rc;
-    }
+    if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
     if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   }
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
   FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
   device_last_compute(ctx->device) = ctx->ev_done;
-  if (!ctx->async_lock || cached_q < 0) FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_done));
+  // a frame with a host round trip inside keeps the lock until it is done
+  if (!ctx->async_lock || (cached_q < 0 && !folded))
+    FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_done));
   compute_lock.unlock();
   NvtxRange nv_out("fgbd.download");
   if (!dev && (rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), false))) return rc;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
   if ((rc = pull_ctl(ctx))) return rc;
   if ((rc = check_graph_ctl(ctx, bits))) return rc;
+  if (cached_q < 0 && folded && (rc = collect_noise(ctx, cfg->patch_size, &nz))) return rc;
   const Ctl& h = *ctx->ctl_host;
   if (want_reuse && !reuse) {  // the copy now describes a complete graph with weights
     ctx->held_edges = h.n_edges;

@@ -85,6 +85,18 @@ struct Ctl {
   // slab ranks: this rank's share before the cross-rank all-gather
   unsigned long long sg_fx[2];  // exact fixed-point sum of edge lengths (k_rows)
   double mask_part[7];          // k_mask totals: count, sum_inc y^2 [3], sum_all y^2 [3]
+  // NE-GBP finished on the device (k_finish_noise): noise.py:122-249
+  int nz_err;                   // NzErr code (0: ok)
+  int nz_err_arg;               // channel / count / degree for the message
+  double nz_err_val;            // off-diagonal norm of a non-converged Jacobi
+  double nz_sigma, nz_pcs[3], nz_eig[3][8], nz_tau[3];
+  int nz_m[3], nz_fb[3], nz_direct[3];
+  double fslr_thr;              // 2 sigma_est
+  int fslr_active;              // FSLR mask on
+};
+
+enum NzErr {
+  NZ_OK = 0, NZ_PATCH = 1, NZ_FEW = 2, NZ_ASYM = 3, NZ_NOCONV = 4, NZ_TAIL_D = 5, NZ_TAIL_SORT = 6
 };
 
 constexpr int kMaxRanks = 16;
@@ -302,6 +314,13 @@ int launch_noise(fgbd_ctx* ctx, int64_t n, int patch, int fuse_weights);
 int launch_noise_slab(fgbd_ctx* ctx, int64_t n_own, int patch, const SlabView& v);
 // host side: covariance -> Jacobi -> tail -> sigma (noise.py:122-243)
 int finish_noise(fgbd_ctx* ctx, int patch, int divisor, fgbd_noise* out);
+// the same on the device, bit for bit (no host round trip): writes the nz_*
+// fields, sv2 and the FSLR threshold into ctl
+int launch_finish_noise(fgbd_ctx* ctx, int patch, int divisor, int fslr_enabled,
+                        double sigma_floor);
+// host: the error k_finish_noise recorded (ctl mirror current), as finish_noise would raise it;
+// otherwise fills *out from the device results
+int collect_noise(fgbd_ctx* ctx, int patch, fgbd_noise* out);
 int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err,
                        int* direct_off);
 int select_tail_host(const double* lam, int d, int divisor, int* m, double* tau,
@@ -319,8 +338,7 @@ int launch_mask_slab(fgbd_ctx* ctx, int64_t n_own, const double4* y, double sigm
 int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64);
 // the FSLR mask (k_mask) folded into the first filter step
 bool mask_foldable(const fgbd_ctx* ctx, int q_max, int w64);
-int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_max,
-                               int mode, int early_exit);
+int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, int q_max, int mode, int early_exit);
 // persistent filter: contiguous row range per block (true) or grid-stride waves
 bool lf_contiguous(const fgbd_ctx* ctx, int64_t rows);
 int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf);

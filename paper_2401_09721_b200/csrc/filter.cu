@@ -199,13 +199,11 @@ struct StepArgs {
   unsigned long long base;    // P2P: this launch's flag base (published value = base + step)
   // FSLR mask folded into step 1 (fold != 0, select_q from denoise): step 1
   // thresholds fslr[] into the mask and sums the select_q initial totals
+  // (sigma_est, the threshold and FSLR on/off are read from ctl: k_finish_noise)
   int fold;
   const double* fslr;
-  double thr;     // 2 sigma_est
-  int active;     // FSLR on (filtering.py:285-295)
   double* xpart;  // [10][grid]: count, sum_inc y^2 [3], sum_all y^2 [3], sum_all x1^2 [3]
   int q_max, mode, early_exit;
-  double sv2;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -431,7 +429,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 template <int WM, bool SUMS, bool FOLD = false>
 __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, double4* out,
                                       bool mask_all, float neg_inv_sg2, double (&sx)[3],
-                                      int4* s_ell, double* xs = nullptr /*[10] with FOLD*/) {
+                                      int4* s_ell, double* xs = nullptr /*[10] with FOLD*/,
+                                      double thr = 0.0, int active = 0) {
   const int64_t n = a.n;
   // rows of this block: a contiguous range walked in blockDim strides (the
   // neighbours of raster / scan-ordered clouds then mostly hit this SM's L1),
@@ -508,7 +507,7 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
     if (FOLD) {
       // k_mask's work for this row (filtering.py:175-194, 237-243): the
       // FSLR bit, and the initial totals over included / all rows
-      const bool inc = !(a.active && a.fslr[i] > a.thr);
+      const bool inc = !(active && a.fslr[i] > thr);
       const unsigned bits = __ballot_sync(__activemask(), inc);
       if ((threadIdx.x & 31) == 0) const_cast<uint32_t*>(a.mask)[i >> 5] = bits;
       const double y2[3] = {f.x * f.x, f.y * f.y, f.z * f.z};
@@ -803,7 +802,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   __shared__ int s_qmax, s_mode, s_early, s_mask_all;
   __shared__ int s_dep_lo, s_dep_hi;
   __shared__ double s_red10[32 * 10];
-  __shared__ int s_fold_stop;
+  __shared__ int s_fold_stop, s_active;
+  __shared__ double s_thr;
   // step c's block partials land here by bulk copy while step c+1 sweeps
   constexpr bool kBulkPart = SELECT && !P2P;
   __shared__ __align__(16) double s_part[kBulkPart ? 3 * kMaxCoopBlocks + 2 : 2];
@@ -836,9 +836,12 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   }
   if (threadIdx.x == 0) {
     if (SELECT && a.fold) {
-      // the mask and the initial totals come out of step 1 (decided at c = 1)
-      s_st = SelState{0, 0, 0, a.q_max <= 0, BUF_Y, BUF_A, BUF_Y, 0.0, 0.0};
-      s_sv2 = a.sv2;
+      // the mask and the initial totals come out of step 1 (decided at c = 1);
+      // sigma_est comes from k_finish_noise, and a noise error stops at once
+      s_st = SelState{0, 0, 0, a.q_max <= 0 || ctl->nz_err != 0, BUF_Y, BUF_A, BUF_Y, 0.0, 0.0};
+      s_sv2 = ctl->sv2;
+      s_thr = ctl->fslr_thr;
+      s_active = ctl->fslr_active;
       s_qmax = a.q_max;
       s_mode = a.mode;
       s_early = a.early_exit;
@@ -896,7 +899,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
         // step 1 also does k_mask's work (FSLR bits + the initial totals)
         double xs[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         sweep<WM, SELECT, true>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx,
-                                s_ell, xs);
+                                s_ell, xs, s_thr, s_active);
         block_sum<10>(xs, s_red10);
         if (threadIdx.x == 0)
           for (int k = 0; k < 10; ++k) a.xpart[k * nb + blockIdx.x] = xs[k];
@@ -952,7 +955,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
         block_sum<10>(x, s_red10);
         if (threadIdx.x == 0) {
           long long cnt = (long long)x[0];
-          const bool all_ex = (cnt == 0) && a.active;
+          const bool all_ex = (cnt == 0) && s_active;
           if (all_ex) cnt = a.n;
           for (int k = 0; k < 3; ++k) s_sy[k] = all_ex ? x[4 + k] : x[1 + k];
           s_inc = cnt;
@@ -1344,18 +1347,14 @@ bool mask_foldable(const fgbd_ctx* ctx, int q_max, int w64) {
   return ctx->mask_fold && ctx->lf_variant == 10 && !w64 && q_max >= 1;
 }
 
-int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, double sigma_est, int active, int q_max,
-                               int mode, int early_exit) {
+int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, int q_max, int mode, int early_exit) {
   StepArgs a = step_args(ctx, n);
-  a.fold = 1;
+  a.fold = 1;  // sigma_est, the FSLR threshold and on/off come from k_finish_noise (ctl)
   a.fslr = ctx->fslr;
-  a.thr = 2.0 * sigma_est;
-  a.active = active;
   a.xpart = ctx->partials + (1 << 18);  // 10 x grid, clear of the step partials
   a.q_max = q_max;
   a.mode = mode;
   a.early_exit = early_exit;
-  a.sv2 = sigma_est * sigma_est;
   return launch_run<W_STORED, true>(ctx, a);
 }
 

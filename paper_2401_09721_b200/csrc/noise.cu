@@ -509,6 +509,335 @@ int select_tail_host(const double* lam, int d, int divisor, int* m_out, double* 
   return FGBD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// device finish: the host code above, operation for operation (explicit
+// round-to-nearest intrinsics, no contraction -- the host build has no FMA),
+// so sigma_est, the eigenvalues and every verdict are bit-identical to it.
+// hypot is glibc's algorithm (dbl-64 e_hypot.c, non-FMA kernel), which is
+// what numpy's np.hypot calls; checked bit-identical to glibc 2.39 on 2e7
+// arguments including the scaled ranges.
+// ---------------------------------------------------------------------------
+
+__device__ double glibc_hypot_kernel(double ax, double ay) {
+  double t1, t2;
+  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+  if (h <= __dmul_rn(2.0, ay)) {
+    const double delta = __dsub_rn(h, ay);
+    t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, delta), ax));
+    t2 = __dmul_rn(__dsub_rn(delta, __dmul_rn(2.0, __dsub_rn(ax, ay))), delta);
+  } else {
+    const double delta = __dsub_rn(h, ax);
+    t1 = __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+    t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, delta), ay), ay), __dmul_rn(delta, delta));
+  }
+  return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+}
+
+__device__ double glibc_hypot(double x, double y) {
+  const double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54;
+  x = fabs(x);
+  y = fabs(y);
+  const double ax = x < y ? y : x, ay = x < y ? x : y;
+  if (ax > kLarge) {
+    if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+    return __ddiv_rn(glibc_hypot_kernel(__dmul_rn(ax, kScale), __dmul_rn(ay, kScale)), kScale);
+  }
+  if (ay < kTiny) {
+    if (ax >= __ddiv_rn(ay, kEps)) return __dadd_rn(ax, ay);
+    return __dmul_rn(glibc_hypot_kernel(__ddiv_rn(ax, kScale), __ddiv_rn(ay, kScale)), kScale);
+  }
+  if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+  return glibc_hypot_kernel(ax, ay);
+}
+
+__device__ double dev_pairwise_sum(const double* x, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, x[i]);
+    return res;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = x[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], x[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, x[i]);
+  return res;
+}
+
+__device__ void dev_sort_desc(double* v, int n) {
+  for (int i = 1; i < n; ++i) {
+    const double x = v[i];
+    int j = i - 1;
+    while (j >= 0 && v[j] < x) {
+      v[j + 1] = v[j];
+      --j;
+    }
+    v[j + 1] = x;
+  }
+}
+
+// jacobi_eigenvalues: 0 ok, NZ_ASYM, NZ_NOCONV (*off_out = the norm)
+__device__ int dev_jacobi(const double* s, int d, double* out, double* off_out, int* direct) {
+  *direct = 0;
+  double scale = 0.0, asym = 0.0;
+  for (int i = 0; i < d * d; ++i) scale = fmax(scale, fabs(s[i]));
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) asym = fmax(asym, fabs(__dsub_rn(s[i * d + j], s[j * d + i])));
+  if (scale > 0 && asym > __dmul_rn(1e-9, scale)) return NZ_ASYM;
+  double a[49];
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) a[i * d + j] = __dmul_rn(__dadd_rn(s[i * d + j], s[j * d + i]), 0.5);
+  double fro2 = 0.0;
+  for (int i = 0; i < d * d; ++i) fro2 = __dadd_rn(fro2, __dmul_rn(a[i], a[i]));
+  const double norm = __dsqrt_rn(fro2);
+  auto finish = [&]() {
+    for (int i = 0; i < d; ++i) out[i] = a[i * d + i];
+    dev_sort_desc(out, d);
+  };
+  if (norm == 0.0 || d == 1) {
+    finish();
+    return 0;
+  }
+  const double target = __dmul_rn(1e-12, norm);
+  auto off_norm = [&]() {
+    double sq[49];
+    for (int i = 0; i < d * d; ++i) sq[i] = __dmul_rn(a[i], a[i]);
+    const double all = dev_pairwise_sum(sq, d * d);
+    double dg = 0.0;
+    for (int i = 0; i < d; ++i) dg = __dadd_rn(dg, __dmul_rn(a[i * d + i], a[i * d + i]));
+    return __dsqrt_rn(fmax(__dsub_rn(all, dg), 0.0));
+  };
+  double cp[7], cq[7];
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    if (off_norm() <= target) {
+      finish();
+      return 0;
+    }
+    for (int p = 0; p < d - 1; ++p) {
+      for (int q = p + 1; q < d; ++q) {
+        const double apq = a[p * d + q];
+        if (apq == 0.0) continue;
+        const double diff = __dsub_rn(a[q * d + q], a[p * d + p]);
+        double t;
+        if (fabs(apq) < __dmul_rn(1e-36, fabs(diff))) {
+          t = __ddiv_rn(apq, diff);
+        } else {
+          const double theta = __ddiv_rn(diff, __dmul_rn(2.0, apq));
+          const double sg = theta > 0 ? 1.0 : (theta < 0 ? -1.0 : 0.0);
+          t = __ddiv_rn(sg, __dadd_rn(fabs(theta), glibc_hypot(theta, 1.0)));
+          if (t == 0.0) t = 1.0;
+        }
+        const double c = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__dmul_rn(t, t), 1.0)));
+        const double sn = __dmul_rn(t, c);
+        for (int i = 0; i < d; ++i) {
+          cp[i] = a[i * d + p];
+          cq[i] = a[i * d + q];
+        }
+        for (int i = 0; i < d; ++i) {
+          a[i * d + p] = __dsub_rn(__dmul_rn(c, cp[i]), __dmul_rn(sn, cq[i]));
+          a[i * d + q] = __dadd_rn(__dmul_rn(sn, cp[i]), __dmul_rn(c, cq[i]));
+        }
+        for (int j = 0; j < d; ++j) {
+          cp[j] = a[p * d + j];
+          cq[j] = a[q * d + j];
+        }
+        for (int j = 0; j < d; ++j) {
+          a[p * d + j] = __dsub_rn(__dmul_rn(c, cp[j]), __dmul_rn(sn, cq[j]));
+          a[q * d + j] = __dadd_rn(__dmul_rn(sn, cp[j]), __dmul_rn(c, cq[j]));
+        }
+        a[p * d + q] = 0.0;
+        a[q * d + p] = 0.0;
+      }
+    }
+  }
+  const double off = off_norm();
+  double off_direct = 0.0;
+  for (int p = 0; p < d; ++p)
+    for (int q = 0; q < d; ++q)
+      if (p != q) off_direct = __dadd_rn(off_direct, __dmul_rn(a[p * d + q], a[p * d + q]));
+  if (off <= target || __dsqrt_rn(off_direct) <= target) {
+    if (!(off <= target)) *direct = 1;
+    finish();
+    return 0;
+  }
+  *off_out = off;
+  return NZ_NOCONV;
+}
+
+__device__ double dev_median(const double* v, int m) {
+  double s[7];
+  for (int i = 0; i < m; ++i) s[i] = v[i];
+  for (int i = 1; i < m; ++i) {  // ascending
+    const double x = s[i];
+    int j = i - 1;
+    while (j >= 0 && s[j] > x) {
+      s[j + 1] = s[j];
+      --j;
+    }
+    s[j + 1] = x;
+  }
+  if (m & 1) return s[m / 2];
+  return __ddiv_rn(__dadd_rn(s[m / 2 - 1], s[m / 2]), 2.0);
+}
+
+// select_tail_host: 0 ok, NZ_TAIL_D, NZ_TAIL_SORT
+__device__ int dev_select_tail(const double* lam, int d, int divisor, int* m_out, double* tau_out,
+                               int* fb_out) {
+  if (d < 3) return NZ_TAIL_D;
+  double scale = 1.0;
+  for (int i = 0; i < d; ++i) scale = fmax(scale, fabs(lam[i]));
+  for (int i = 0; i + 1 < d; ++i)
+    if (__dsub_rn(lam[i + 1], lam[i]) > __dmul_rn(1e-9, scale)) return NZ_TAIL_SORT;
+  const int extra = divisor == FGBD_TAU_COUNT ? 0 : 1;
+  auto tail_tau = [&](int m) {
+    double s = 0.0;
+    for (int k = m; k < d; ++k) s = __dadd_rn(s, lam[k]);
+    return __ddiv_rn(s, (double)(d - m + extra));
+  };
+  for (int m = 1; m < d - 1; ++m) {
+    const double tau = tail_tau(m);
+    if (tau > dev_median(lam + m, d - m)) {
+      *m_out = m;
+      *tau_out = tau;
+      *fb_out = 0;
+      return 0;
+    }
+  }
+  const int m = d / 2;
+  *m_out = m;
+  *tau_out = tail_tau(m);
+  *fb_out = 1;
+  return 0;
+}
+
+// One block of 32 threads; threads 0..2 finish one colour channel each.
+__global__ void __launch_bounds__(32) k_finish_noise(Ctl* ctl, int D, int divisor,
+                                                     int fslr_enabled, double sigma_floor) {
+  __shared__ int s_err[3];
+  __shared__ double s_off[3];
+  const int c = threadIdx.x;
+  const long long ne = ctl->eligible;
+  if (c < 3) {
+    s_err[c] = 0;
+    if (ne >= 2 && D <= 1 + ctl->max_deg) {
+      const double* G = ctl->gram[c];
+      double mu[7], cov[49], lam[7];
+      for (int k = 0; k < D; ++k) mu[k] = __ddiv_rn(G[k * 8 + 7], (double)ne);
+      for (int k = 0; k < D; ++k)
+        for (int l = k; l < D; ++l) {
+          const double v = __dsub_rn(__ddiv_rn(G[k * 8 + l], (double)ne), __dmul_rn(mu[k], mu[l]));
+          cov[k * D + l] = v;
+          cov[l * D + k] = v;
+        }
+      double off = 0.0;
+      int direct = 0;
+      int e = dev_jacobi(cov, D, lam, &off, &direct);
+      int m = 0, fb = 0;
+      double tau = 0.0;
+      if (!e) e = dev_select_tail(lam, D, divisor, &m, &tau, &fb);
+      s_err[c] = e;
+      s_off[c] = off;
+      if (!e) {
+        for (int k = 0; k < D; ++k) ctl->nz_eig[c][k] = lam[k];
+        ctl->nz_m[c] = m;
+        ctl->nz_tau[c] = tau;
+        ctl->nz_fb[c] = fb;
+        ctl->nz_direct[c] = direct;
+        ctl->nz_pcs[c] = __dsqrt_rn(fmax(tau, 0.0));
+      }
+    }
+  }
+  __syncthreads();
+  if (c == 0) {
+    int err = 0, arg = 0;
+    double val = 0.0;
+    if (D > 1 + ctl->max_deg) {
+      err = NZ_PATCH;
+      arg = 1 + ctl->max_deg;
+    } else if (ne < 2) {
+      err = NZ_FEW;
+      arg = (int)ne;
+    } else {
+      for (int k = 0; k < 3 && !err; ++k)
+        if (s_err[k]) {
+          err = s_err[k];
+          arg = k;
+          val = s_off[k];
+        }
+    }
+    ctl->nz_err = err;
+    ctl->nz_err_arg = arg;
+    ctl->nz_err_val = val;
+    if (!err) {
+      const double sig =
+          __ddiv_rn(__dadd_rn(__dadd_rn(ctl->nz_pcs[0], ctl->nz_pcs[1]), ctl->nz_pcs[2]), 3.0);
+      ctl->nz_sigma = sig;
+      ctl->sv2 = __dmul_rn(sig, sig);
+      ctl->fslr_thr = __dmul_rn(2.0, sig);
+      ctl->fslr_active = fslr_enabled && !(sig < sigma_floor);
+    }
+  }
+}
+
+int launch_finish_noise(fgbd_ctx* ctx, int patch, int divisor, int fslr_enabled,
+                        double sigma_floor) {
+  k_finish_noise<<<1, 32, 0, ctx->stream>>>(ctx->ctl, patch, divisor, fslr_enabled, sigma_floor);
+  FGBD_LAUNCH(ctx);
+  return FGBD_OK;
+}
+
+int collect_noise(fgbd_ctx* ctx, int D, fgbd_noise* out) {
+  const Ctl& h = *ctx->ctl_host;
+  std::memset(out, 0, sizeof(*out));
+  out->patch_size = D;
+  out->eligible_count = h.eligible;
+  switch (h.nz_err) {
+    case NZ_OK:
+      break;
+    case NZ_PATCH:
+      return set_error(ctx, FGBD_E_NOISE, "patch_size " + std::to_string(D) +
+                                              " exceeds 1 + max degree (" +
+                                              std::to_string(h.nz_err_arg) + ") of this graph");
+    case NZ_FEW:
+      return set_error(ctx, FGBD_E_NOISE,
+                       "need at least 2 patches, have " + std::to_string(h.eligible));
+    case NZ_ASYM:
+      return set_error(ctx, FGBD_E_NOISE, "matrix is not symmetric within tolerance");
+    case NZ_NOCONV: {
+      char buf[128];
+      std::snprintf(buf, sizeof(buf), "Jacobi did not converge in 50 sweeps (off-diagonal %.3e)",
+                    h.nz_err_val);
+      return set_error(ctx, FGBD_E_NOISE, buf);
+    }
+    case NZ_TAIL_D:
+      return set_error(ctx, FGBD_E_NOISE, "need at least 3 eigenvalues, got " + std::to_string(D));
+    default:
+      return set_error(ctx, FGBD_E_NOISE, "eigenvalues must be sorted descending");
+  }
+  for (int c = 0; c < 3; ++c) {
+    const double* G = h.gram[c];
+    double mu[7];
+    for (int k = 0; k < D; ++k) mu[k] = G[k * 8 + 7] / (double)h.eligible;
+    for (int k = 0; k < D; ++k)
+      for (int l = k; l < D; ++l) {
+        const double v = G[k * 8 + l] / (double)h.eligible - mu[k] * mu[l];
+        out->covariance[c][k][l] = v;
+        out->covariance[c][l][k] = v;
+      }
+    for (int k = 0; k < D; ++k) out->eigenvalues[c][k] = h.nz_eig[c][k];
+    out->m[c] = h.nz_m[c];
+    out->tau[c] = h.nz_tau[c];
+    out->fallback[c] = h.nz_fb[c];
+    out->jacobi_direct_off[c] = h.nz_direct[c];
+    out->per_channel_sigma[c] = h.nz_pcs[c];
+  }
+  out->sigma_est = h.nz_sigma;
+  return FGBD_OK;
+}
+
 // Reads the reduced moments (ctl mirror must be current) and finishes
 // noise.py:122-243 on the host.
 int finish_noise(fgbd_ctx* ctx, int D, int divisor, fgbd_noise* out) {
