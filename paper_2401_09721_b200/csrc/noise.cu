@@ -550,114 +550,135 @@ __device__ double glibc_hypot(double x, double y) {
   return glibc_hypot_kernel(ax, ay);
 }
 
-__device__ double dev_pairwise_sum(const double* x, int n) {
-  if (n < 8) {
+// numpy's add.reduce of N <= 49 values (pairwise_sum, 8 accumulators)
+template <int N>
+__device__ __forceinline__ double dev_pairwise_sum(const double (&x)[N]) {
+  if (N < 8) {
     double res = 0.0;
-    for (int i = 0; i < n; ++i) res = __dadd_rn(res, x[i]);
+#pragma unroll
+    for (int i = 0; i < N; ++i) res = __dadd_rn(res, x[i]);
     return res;
   }
   double r[8];
-  for (int j = 0; j < 8; ++j) r[j] = x[j];
-  int i = 8;
-  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = x[j < N ? j : 0];
+  constexpr int kBody = N - (N % 8);
+#pragma unroll
+  for (int i = 8; i < kBody; i += 8)
+#pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], x[i + j]);
   double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) res = __dadd_rn(res, x[i]);
+#pragma unroll
+  for (int i = kBody; i < N; ++i) res = __dadd_rn(res, x[i]);
   return res;
 }
 
-__device__ void dev_sort_desc(double* v, int n) {
-  for (int i = 1; i < n; ++i) {
-    const double x = v[i];
-    int j = i - 1;
-    while (j >= 0 && v[j] < x) {
-      v[j + 1] = v[j];
-      --j;
-    }
-    v[j + 1] = x;
-  }
+template <int D>
+__device__ __forceinline__ void dev_sort_desc(double (&v)[D]) {
+#pragma unroll
+  for (int i = 1; i < D; ++i)
+#pragma unroll
+    for (int j = i; j > 0; --j)
+      if (v[j - 1] < v[j]) {  // insertion sort as a fixed network of swaps
+        const double t = v[j - 1];
+        v[j - 1] = v[j];
+        v[j] = t;
+      }
 }
 
-// jacobi_eigenvalues: 0 ok, NZ_ASYM, NZ_NOCONV (*off_out = the norm)
-__device__ int dev_jacobi(const double* s, int d, double* out, double* off_out, int* direct) {
+// jacobi_eigenvalues for a D x D matrix held in registers: 0 ok, NZ_ASYM,
+// NZ_NOCONV (*off_out = the norm)
+template <int D>
+__device__ int dev_jacobi(const double (&s)[D * D], double (&out)[D], double* off_out,
+                          int* direct) {
   *direct = 0;
   double scale = 0.0, asym = 0.0;
-  for (int i = 0; i < d * d; ++i) scale = fmax(scale, fabs(s[i]));
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j) asym = fmax(asym, fabs(__dsub_rn(s[i * d + j], s[j * d + i])));
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) scale = fmax(scale, fabs(s[i]));
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) asym = fmax(asym, fabs(__dsub_rn(s[i * D + j], s[j * D + i])));
   if (scale > 0 && asym > __dmul_rn(1e-9, scale)) return NZ_ASYM;
-  double a[49];
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j) a[i * d + j] = __dmul_rn(__dadd_rn(s[i * d + j], s[j * d + i]), 0.5);
+  double a[D * D];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) a[i * D + j] = __dmul_rn(__dadd_rn(s[i * D + j], s[j * D + i]), 0.5);
   double fro2 = 0.0;
-  for (int i = 0; i < d * d; ++i) fro2 = __dadd_rn(fro2, __dmul_rn(a[i], a[i]));
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) fro2 = __dadd_rn(fro2, __dmul_rn(a[i], a[i]));
   const double norm = __dsqrt_rn(fro2);
   auto finish = [&]() {
-    for (int i = 0; i < d; ++i) out[i] = a[i * d + i];
-    dev_sort_desc(out, d);
+#pragma unroll
+    for (int i = 0; i < D; ++i) out[i] = a[i * D + i];
+    dev_sort_desc<D>(out);
   };
-  if (norm == 0.0 || d == 1) {
+  if (norm == 0.0 || D == 1) {
     finish();
     return 0;
   }
   const double target = __dmul_rn(1e-12, norm);
   auto off_norm = [&]() {
-    double sq[49];
-    for (int i = 0; i < d * d; ++i) sq[i] = __dmul_rn(a[i], a[i]);
-    const double all = dev_pairwise_sum(sq, d * d);
+    double sq[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) sq[i] = __dmul_rn(a[i], a[i]);
+    const double all = dev_pairwise_sum<D * D>(sq);
     double dg = 0.0;
-    for (int i = 0; i < d; ++i) dg = __dadd_rn(dg, __dmul_rn(a[i * d + i], a[i * d + i]));
+#pragma unroll
+    for (int i = 0; i < D; ++i) dg = __dadd_rn(dg, __dmul_rn(a[i * D + i], a[i * D + i]));
     return __dsqrt_rn(fmax(__dsub_rn(all, dg), 0.0));
   };
-  double cp[7], cq[7];
+#pragma unroll 1
   for (int sweep = 0; sweep < 50; ++sweep) {
     if (off_norm() <= target) {
       finish();
       return 0;
     }
-    for (int p = 0; p < d - 1; ++p) {
-      for (int q = p + 1; q < d; ++q) {
-        const double apq = a[p * d + q];
-        if (apq == 0.0) continue;
-        const double diff = __dsub_rn(a[q * d + q], a[p * d + p]);
-        double t;
-        if (fabs(apq) < __dmul_rn(1e-36, fabs(diff))) {
-          t = __ddiv_rn(apq, diff);
-        } else {
-          const double theta = __ddiv_rn(diff, __dmul_rn(2.0, apq));
-          const double sg = theta > 0 ? 1.0 : (theta < 0 ? -1.0 : 0.0);
-          t = __ddiv_rn(sg, __dadd_rn(fabs(theta), glibc_hypot(theta, 1.0)));
-          if (t == 0.0) t = 1.0;
+#pragma unroll
+    for (int p = 0; p < D - 1; ++p) {
+#pragma unroll
+      for (int q = p + 1; q < D; ++q) {
+        const double apq = a[p * D + q];
+        if (apq != 0.0) {
+          const double diff = __dsub_rn(a[q * D + q], a[p * D + p]);
+          double t;
+          if (fabs(apq) < __dmul_rn(1e-36, fabs(diff))) {
+            t = __ddiv_rn(apq, diff);
+          } else {
+            const double theta = __ddiv_rn(diff, __dmul_rn(2.0, apq));
+            const double sg = theta > 0 ? 1.0 : (theta < 0 ? -1.0 : 0.0);
+            t = __ddiv_rn(sg, __dadd_rn(fabs(theta), glibc_hypot(theta, 1.0)));
+            if (t == 0.0) t = 1.0;
+          }
+          const double c = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__dmul_rn(t, t), 1.0)));
+          const double sn = __dmul_rn(t, c);
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const double cp = a[i * D + p], cq = a[i * D + q];
+            a[i * D + p] = __dsub_rn(__dmul_rn(c, cp), __dmul_rn(sn, cq));
+            a[i * D + q] = __dadd_rn(__dmul_rn(sn, cp), __dmul_rn(c, cq));
+          }
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const double cp = a[p * D + j], cq = a[q * D + j];
+            a[p * D + j] = __dsub_rn(__dmul_rn(c, cp), __dmul_rn(sn, cq));
+            a[q * D + j] = __dadd_rn(__dmul_rn(sn, cp), __dmul_rn(c, cq));
+          }
+          a[p * D + q] = 0.0;
+          a[q * D + p] = 0.0;
         }
-        const double c = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__dmul_rn(t, t), 1.0)));
-        const double sn = __dmul_rn(t, c);
-        for (int i = 0; i < d; ++i) {
-          cp[i] = a[i * d + p];
-          cq[i] = a[i * d + q];
-        }
-        for (int i = 0; i < d; ++i) {
-          a[i * d + p] = __dsub_rn(__dmul_rn(c, cp[i]), __dmul_rn(sn, cq[i]));
-          a[i * d + q] = __dadd_rn(__dmul_rn(sn, cp[i]), __dmul_rn(c, cq[i]));
-        }
-        for (int j = 0; j < d; ++j) {
-          cp[j] = a[p * d + j];
-          cq[j] = a[q * d + j];
-        }
-        for (int j = 0; j < d; ++j) {
-          a[p * d + j] = __dsub_rn(__dmul_rn(c, cp[j]), __dmul_rn(sn, cq[j]));
-          a[q * d + j] = __dadd_rn(__dmul_rn(sn, cp[j]), __dmul_rn(c, cq[j]));
-        }
-        a[p * d + q] = 0.0;
-        a[q * d + p] = 0.0;
       }
     }
   }
   const double off = off_norm();
   double off_direct = 0.0;
-  for (int p = 0; p < d; ++p)
-    for (int q = 0; q < d; ++q)
-      if (p != q) off_direct = __dadd_rn(off_direct, __dmul_rn(a[p * d + q], a[p * d + q]));
+#pragma unroll
+  for (int p = 0; p < D; ++p)
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+      if (p != q) off_direct = __dadd_rn(off_direct, __dmul_rn(a[p * D + q], a[p * D + q]));
   if (off <= target || __dsqrt_rn(off_direct) <= target) {
     if (!(off <= target)) *direct = 1;
     finish();
@@ -667,50 +688,109 @@ __device__ int dev_jacobi(const double* s, int d, double* out, double* off_out, 
   return NZ_NOCONV;
 }
 
-__device__ double dev_median(const double* v, int m) {
-  double s[7];
-  for (int i = 0; i < m; ++i) s[i] = v[i];
-  for (int i = 1; i < m; ++i) {  // ascending
-    const double x = s[i];
-    int j = i - 1;
-    while (j >= 0 && s[j] > x) {
-      s[j + 1] = s[j];
-      --j;
-    }
-    s[j + 1] = x;
+template <int M>
+__device__ __forceinline__ double dev_median(const double* v) {
+  double s[M];
+#pragma unroll
+  for (int i = 0; i < M; ++i) s[i] = v[i];
+#pragma unroll
+  for (int i = 1; i < M; ++i)  // ascending
+#pragma unroll
+    for (int j = i; j > 0; --j)
+      if (s[j - 1] > s[j]) {
+        const double t = s[j - 1];
+        s[j - 1] = s[j];
+        s[j] = t;
+      }
+  if (M & 1) return s[M / 2];
+  return __ddiv_rn(__dadd_rn(s[M / 2 - 1], s[M / 2]), 2.0);
+}
+
+template <int D, int M>
+__device__ __forceinline__ bool tail_step(const double (&lam)[D], int extra, int* m_out,
+                                          double* tau_out) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = M; k < D; ++k) s = __dadd_rn(s, lam[k]);
+  const double tau = __ddiv_rn(s, (double)(D - M + extra));
+  if (tau > dev_median<D - M>(lam + M)) {
+    *m_out = M;
+    *tau_out = tau;
+    return true;
   }
-  if (m & 1) return s[m / 2];
-  return __ddiv_rn(__dadd_rn(s[m / 2 - 1], s[m / 2]), 2.0);
+  return false;
 }
 
 // select_tail_host: 0 ok, NZ_TAIL_D, NZ_TAIL_SORT
-__device__ int dev_select_tail(const double* lam, int d, int divisor, int* m_out, double* tau_out,
+template <int D>
+__device__ int dev_select_tail(const double (&lam)[D], int divisor, int* m_out, double* tau_out,
                                int* fb_out) {
-  if (d < 3) return NZ_TAIL_D;
+  if (D < 3) return NZ_TAIL_D;
   double scale = 1.0;
-  for (int i = 0; i < d; ++i) scale = fmax(scale, fabs(lam[i]));
-  for (int i = 0; i + 1 < d; ++i)
+#pragma unroll
+  for (int i = 0; i < D; ++i) scale = fmax(scale, fabs(lam[i]));
+#pragma unroll
+  for (int i = 0; i + 1 < D; ++i)
     if (__dsub_rn(lam[i + 1], lam[i]) > __dmul_rn(1e-9, scale)) return NZ_TAIL_SORT;
   const int extra = divisor == FGBD_TAU_COUNT ? 0 : 1;
-  auto tail_tau = [&](int m) {
-    double s = 0.0;
-    for (int k = m; k < d; ++k) s = __dadd_rn(s, lam[k]);
-    return __ddiv_rn(s, (double)(d - m + extra));
-  };
-  for (int m = 1; m < d - 1; ++m) {
-    const double tau = tail_tau(m);
-    if (tau > dev_median(lam + m, d - m)) {
-      *m_out = m;
-      *tau_out = tau;
-      *fb_out = 0;
-      return 0;
-    }
+  *fb_out = 0;
+  // smallest m in [1, D-2] with mean(tail) > median(tail) (noise.py:188-216)
+  if constexpr (D >= 3) {
+    if (tail_step<D, 1>(lam, extra, m_out, tau_out)) return 0;
   }
-  const int m = d / 2;
+  if constexpr (D >= 4) {
+    if (tail_step<D, 2>(lam, extra, m_out, tau_out)) return 0;
+  }
+  if constexpr (D >= 5) {
+    if (tail_step<D, 3>(lam, extra, m_out, tau_out)) return 0;
+  }
+  if constexpr (D >= 6) {
+    if (tail_step<D, 4>(lam, extra, m_out, tau_out)) return 0;
+  }
+  if constexpr (D >= 7) {
+    if (tail_step<D, 5>(lam, extra, m_out, tau_out)) return 0;
+  }
+  constexpr int m = D / 2;
+  double s = 0.0;
+#pragma unroll
+  for (int k = m; k < D; ++k) s = __dadd_rn(s, lam[k]);
   *m_out = m;
-  *tau_out = tail_tau(m);
+  *tau_out = __ddiv_rn(s, (double)(D - m + extra));
   *fb_out = 1;
   return 0;
+}
+
+// one colour channel: covariance from the Gram moments, Jacobi, tail rule
+template <int D>
+__device__ void finish_channel(Ctl* ctl, int c, long long ne, int divisor, int* err,
+                               double* off) {
+  const double* G = ctl->gram[c];
+  double mu[D], cov[D * D], lam[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) mu[k] = __ddiv_rn(G[k * 8 + 7], (double)ne);
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+#pragma unroll
+    for (int l = k; l < D; ++l) {
+      const double v = __dsub_rn(__ddiv_rn(G[k * 8 + l], (double)ne), __dmul_rn(mu[k], mu[l]));
+      cov[k * D + l] = v;
+      cov[l * D + k] = v;
+    }
+  int direct = 0;
+  int e = dev_jacobi<D>(cov, lam, off, &direct);
+  int m = 0, fb = 0;
+  double tau = 0.0;
+  if (!e) e = dev_select_tail<D>(lam, divisor, &m, &tau, &fb);
+  *err = e;
+  if (!e) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) ctl->nz_eig[c][k] = lam[k];
+    ctl->nz_m[c] = m;
+    ctl->nz_tau[c] = tau;
+    ctl->nz_fb[c] = fb;
+    ctl->nz_direct[c] = direct;
+    ctl->nz_pcs[c] = __dsqrt_rn(fmax(tau, 0.0));
+  }
 }
 
 // One block of 32 threads; threads 0..2 finish one colour channel each.
@@ -721,34 +801,20 @@ __global__ void __launch_bounds__(32) k_finish_noise(Ctl* ctl, int D, int diviso
   const int c = threadIdx.x;
   const long long ne = ctl->eligible;
   if (c < 3) {
-    s_err[c] = 0;
+    int e = 0;
+    double off = 0.0;
     if (ne >= 2 && D <= 1 + ctl->max_deg) {
-      const double* G = ctl->gram[c];
-      double mu[7], cov[49], lam[7];
-      for (int k = 0; k < D; ++k) mu[k] = __ddiv_rn(G[k * 8 + 7], (double)ne);
-      for (int k = 0; k < D; ++k)
-        for (int l = k; l < D; ++l) {
-          const double v = __dsub_rn(__ddiv_rn(G[k * 8 + l], (double)ne), __dmul_rn(mu[k], mu[l]));
-          cov[k * D + l] = v;
-          cov[l * D + k] = v;
-        }
-      double off = 0.0;
-      int direct = 0;
-      int e = dev_jacobi(cov, D, lam, &off, &direct);
-      int m = 0, fb = 0;
-      double tau = 0.0;
-      if (!e) e = dev_select_tail(lam, D, divisor, &m, &tau, &fb);
-      s_err[c] = e;
-      s_off[c] = off;
-      if (!e) {
-        for (int k = 0; k < D; ++k) ctl->nz_eig[c][k] = lam[k];
-        ctl->nz_m[c] = m;
-        ctl->nz_tau[c] = tau;
-        ctl->nz_fb[c] = fb;
-        ctl->nz_direct[c] = direct;
-        ctl->nz_pcs[c] = __dsqrt_rn(fmax(tau, 0.0));
+      switch (D) {
+        case 2: finish_channel<2>(ctl, c, ne, divisor, &e, &off); break;
+        case 3: finish_channel<3>(ctl, c, ne, divisor, &e, &off); break;
+        case 4: finish_channel<4>(ctl, c, ne, divisor, &e, &off); break;
+        case 5: finish_channel<5>(ctl, c, ne, divisor, &e, &off); break;
+        case 6: finish_channel<6>(ctl, c, ne, divisor, &e, &off); break;
+        default: finish_channel<7>(ctl, c, ne, divisor, &e, &off); break;
       }
     }
+    s_err[c] = e;
+    s_off[c] = off;
   }
   __syncthreads();
   if (c == 0) {
