@@ -65,6 +65,13 @@ enum {
  * colours over PCIe.  Without a held graph it behaves as REUSE_GRAPH.  A
  * caller that breaks the guarantee gets the held graph's results. */
 #define FGBD_FLAG_STATIC_GEOMETRY 0x10u
+/* fgbd_denoise: finish NE-GBP (covariance, Jacobi, tail rule) on the device,
+ * bit-identical to the host finish (csrc/noise.cu k_finish_noise, glibc's
+ * hypot reproduced).  A head frame then needs no host round trip and frees
+ * the device for the next frame at enqueue -- a throughput win for
+ * concurrent frames, though one frame alone is ~0.1 ms slower (the 7x7 fp64
+ * Jacobi runs on one thread per channel). */
+#define FGBD_FLAG_DEVICE_NE 0x20u
 
 enum { FGBD_CRIT_POOLED = 0, FGBD_CRIT_PER_CHANNEL = 1 };   /* filtering.py:47 */
 enum { FGBD_TAU_COUNT = 0, FGBD_TAU_COUNT_PLUS_ONE = 1 };   /* filtering.py:49 */

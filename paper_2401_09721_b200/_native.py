@@ -28,6 +28,7 @@ SLAB_EMULATED = 0x1
 SLAB_FULL_OUTPUT = 0x2
 FLAG_REUSE_GRAPH = 0x8
 FLAG_STATIC_GEOMETRY = 0x10
+FLAG_DEVICE_NE = 0x20
 MAX_PATCH = 7
 TRACE_MAX = 1025
 

@@ -622,7 +622,8 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
 
   fgbd_noise nz;
   std::memset(&nz, 0, sizeof(nz));
-  bool folded = false;  // NE finished on the device + the mask folded into the filter
+  bool folded = false;     // the FSLR mask folded into the first filter step
+  bool device_ne = false;  // NE finished on the device (FGBD_FLAG_DEVICE_NE)
   if (cached_q >= 0) {
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
     int fin = BUF_Y;
@@ -638,8 +639,9 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
       ctx->g_weights64 = 0;
     }
     folded = mask_foldable(ctx, cfg->q_max, w64);
+    device_ne = folded && (flags & FGBD_FLAG_DEVICE_NE);
   }
-  if (cached_q < 0 && folded) {
+  if (cached_q < 0 && device_ne) {
     // the whole frame without a host round trip: NE finished on the device
     // (bit-identical to finish_noise), the FSLR mask built by step 1
     if ((rc = launch_finish_noise(ctx, cfg->patch_size, cfg->tau_divisor, cfg->fslr_enabled,
@@ -647,7 +649,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
       return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
     if ((rc = launch_select_steps_folded(ctx, n, cfg->q_max, cfg->criterion_mode,
-                                         cfg->early_exit)))
+                                         cfg->early_exit, nullptr, 0)))
       return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
     if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
@@ -663,11 +665,17 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = finish_noise(ctx, D, cfg->tau_divisor, &nz))) return rc;
     const double sig = nz.sigma_est;
     const int active = cfg->fslr_enabled && !(sig < cfg->fslr_sigma_floor);
-    if ((rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode, cfg->early_exit,
-                          nullptr)))
+    if (!folded && (rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode,
+                                     cfg->early_exit, nullptr)))
       return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
-    if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) return rc;
+    if (folded) {
+      if ((rc = launch_select_steps_folded(ctx, n, cfg->q_max, cfg->criterion_mode,
+                                           cfg->early_exit, &sig, active)))
+        return rc;
+    } else if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) {
+      return rc;
+    }
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[6], ctx->stream));
     if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   }
@@ -675,7 +683,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
   device_last_compute(ctx->device) = ctx->ev_done;
   // a frame with a host round trip inside keeps the lock until it is done
-  if (!ctx->async_lock || (cached_q < 0 && !folded))
+  if (!ctx->async_lock || (cached_q < 0 && !device_ne))
     FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_done));
   compute_lock.unlock();
   NvtxRange nv_out("fgbd.download");
@@ -683,7 +691,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
   if ((rc = pull_ctl(ctx))) return rc;
   if ((rc = check_graph_ctl(ctx, bits))) return rc;
-  if (cached_q < 0 && folded && (rc = collect_noise(ctx, cfg->patch_size, &nz))) return rc;
+  if (cached_q < 0 && device_ne && (rc = collect_noise(ctx, cfg->patch_size, &nz))) return rc;
   const Ctl& h = *ctx->ctl_host;
   if (want_reuse && !reuse) {  // the copy now describes a complete graph with weights
     ctx->held_edges = h.n_edges;

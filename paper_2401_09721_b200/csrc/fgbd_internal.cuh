@@ -338,7 +338,8 @@ int launch_mask_slab(fgbd_ctx* ctx, int64_t n_own, const double4* y, double sigm
 int launch_select_steps(fgbd_ctx* ctx, int64_t n, int q_max, int w64);
 // the FSLR mask (k_mask) folded into the first filter step
 bool mask_foldable(const fgbd_ctx* ctx, int q_max, int w64);
-int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, int q_max, int mode, int early_exit);
+int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, int q_max, int mode, int early_exit,
+                               const double* sigma_est, int active);
 // persistent filter: contiguous row range per block (true) or grid-stride waves
 bool lf_contiguous(const fgbd_ctx* ctx, int64_t rows);
 int launch_fixed_steps(fgbd_ctx* ctx, int64_t n, int q, int w64, int* final_buf);

@@ -199,11 +199,12 @@ struct StepArgs {
   unsigned long long base;    // P2P: this launch's flag base (published value = base + step)
   // FSLR mask folded into step 1 (fold != 0, select_q from denoise): step 1
   // thresholds fslr[] into the mask and sums the select_q initial totals
-  // (sigma_est, the threshold and FSLR on/off are read from ctl: k_finish_noise)
-  int fold;
+  int fold;       // 1: sigma_est etc. below; 2: read from ctl (k_finish_noise)
   const double* fslr;
   double* xpart;  // [10][grid]: count, sum_inc y^2 [3], sum_all y^2 [3], sum_all x1^2 [3]
   int q_max, mode, early_exit;
+  double sv2, thr;  // sigma_est^2, 2 sigma_est
+  int active;       // FSLR on (filtering.py:285-295)
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -838,10 +839,12 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     if (SELECT && a.fold) {
       // the mask and the initial totals come out of step 1 (decided at c = 1);
       // sigma_est comes from k_finish_noise, and a noise error stops at once
-      s_st = SelState{0, 0, 0, a.q_max <= 0 || ctl->nz_err != 0, BUF_Y, BUF_A, BUF_Y, 0.0, 0.0};
-      s_sv2 = ctl->sv2;
-      s_thr = ctl->fslr_thr;
-      s_active = ctl->fslr_active;
+      const bool dev_ne = a.fold == 2;
+      s_st = SelState{0, 0, 0, a.q_max <= 0 || (dev_ne && ctl->nz_err != 0), BUF_Y, BUF_A, BUF_Y,
+                      0.0, 0.0};
+      s_sv2 = dev_ne ? ctl->sv2 : a.sv2;
+      s_thr = dev_ne ? ctl->fslr_thr : a.thr;
+      s_active = dev_ne ? ctl->fslr_active : a.active;
       s_qmax = a.q_max;
       s_mode = a.mode;
       s_early = a.early_exit;
@@ -1347,9 +1350,16 @@ bool mask_foldable(const fgbd_ctx* ctx, int q_max, int w64) {
   return ctx->mask_fold && ctx->lf_variant == 10 && !w64 && q_max >= 1;
 }
 
-int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, int q_max, int mode, int early_exit) {
+int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, int q_max, int mode, int early_exit,
+                               const double* sigma_est, int active) {
   StepArgs a = step_args(ctx, n);
-  a.fold = 1;  // sigma_est, the FSLR threshold and on/off come from k_finish_noise (ctl)
+  // sigma_est given: the host finished NE; null: k_finish_noise left it in ctl
+  a.fold = sigma_est ? 1 : 2;
+  if (sigma_est) {
+    a.sv2 = *sigma_est * *sigma_est;
+    a.thr = 2.0 * *sigma_est;
+    a.active = active;
+  }
   a.fslr = ctx->fslr;
   a.xpart = ctx->partials + (1 << 18);  // 10 x grid, clear of the step partials
   a.q_max = q_max;

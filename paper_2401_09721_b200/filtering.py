@@ -270,15 +270,17 @@ def denoise(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
 
 def denoise_frame(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
                   cached_q: int | None = None, cached_sigma_est: float | None = None,
-                  reuse_graph: bool = False,
-                  static_geometry: bool = False) -> tuple[PointCloud, DenoiseReport]:
+                  reuse_graph: bool = False, static_geometry: bool = False,
+                  device_ne: bool = False) -> tuple[PointCloud, DenoiseReport]:
     """`denoise` for one frame of a sequence.  With `reuse_graph`, a frame
     whose coordinates are byte-identical to the previous frame handled by
     this thread's device context reuses that scan-line graph instead of
     rebuilding it (verified on the device; results are identical).  With
     `static_geometry` the caller GUARANTEES the coordinates equal those of
     the graph this thread's context holds: they are not uploaded or compared
-    (FGBD_FLAG_STATIC_GEOMETRY); without a held graph it acts as reuse_graph."""
+    (FGBD_FLAG_STATIC_GEOMETRY); without a held graph it acts as reuse_graph.
+    `device_ne` finishes NE-GBP on the device (FGBD_FLAG_DEVICE_NE, same bits):
+    no host round trip, so concurrent frames overlap better."""
     n = pc_noisy.n_points
     if n < 2:
         return pc_noisy, DenoiseReport(
@@ -296,7 +298,8 @@ def denoise_frame(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
     ctx.check(ctx.lib.fgbd_denoise(ctx.handle, nat.ptr(pc_noisy.coords), nat.ptr(pc_noisy.colors),
                                    n, bits, nat.make_config(cfg), cq, cs, nat.ptr(out), rep,
                                    (nat.FLAG_REUSE_GRAPH if reuse_graph else 0)
-                                   | (nat.FLAG_STATIC_GEOMETRY if static_geometry else 0)),
+                                   | (nat.FLAG_STATIC_GEOMETRY if static_geometry else 0)
+                                   | (nat.FLAG_DEVICE_NE if device_ne else 0)),
               "denoise")
     report = _report_from(rep, cfg, cached_q, cached_sigma_est)
     out.flags.writeable = False

@@ -99,8 +99,10 @@ def denoise_sequence(frames: Sequence[PointCloud] | Callable[[int], PointCloud],
     host->device bytes (FGBD_FLAG_STATIC_GEOMETRY).
     """
     if denoise_fn is None:
+        # several workers share the GPU: head frames finish NE on the device
+        # so no frame holds the device across a host round trip
         denoise_fn = partial(denoise_frame, reuse_graph=reuse_graph,
-                             static_geometry=static_geometry)
+                             static_geometry=static_geometry, device_ne=workers > 1)
     load = frames if callable(frames) else (lambda i: frames[i])
     n = n_frames if n_frames is not None else len(frames)  # type: ignore[arg-type]
     world, rank = 1, 0

@@ -1,9 +1,10 @@
-"""The NE-GBP finish on the device (k_finish_noise: covariance -> Jacobi ->
-tail rule -> sigma, csrc/noise.cu) against the host C++ finish it replaces
-on the denoise path (FGBD_MASK_FOLD=0 keeps the host round trip): the same
-moments in, bit-identical eigenvalues, tail choices, sigma_est and q out,
-including glibc's hypot reproduced on the device.  Errors keep their class
-and message."""
+"""The NE-GBP finish on the device (FGBD_FLAG_DEVICE_NE, k_finish_noise:
+covariance -> Jacobi -> tail rule -> sigma, csrc/noise.cu) against the host
+C++ finish of the default path: the same moments in, bit-identical
+eigenvalues, tail choices, sigma_est and q out, including glibc's hypot
+reproduced on the device.  Errors keep their class and message.  The
+k_mask path (FGBD_MASK_FOLD=0) is checked the same way against the folded
+mask."""
 
 from __future__ import annotations
 
@@ -14,6 +15,7 @@ import numpy as np
 import pytest
 
 import paper_2401_09721_b200 as fb
+from paper_2401_09721_b200.filtering import denoise_frame
 
 pytestmark = pytest.mark.gpu
 
@@ -56,8 +58,12 @@ def test_device_finish_matches_host_finish(gpu_ready, kind, n, sigma, kw):
     clean, _ = fb.generate_cloud(kind, n, seed=2)
     pc = fb.add_gaussian_noise(clean, sigma, seed=5) if sigma else clean
     cfg = fb.FilterConfig(**kw)
-    dev = _in_thread(lambda: fb.denoise(pc, cfg))
-    host = _in_thread(lambda: fb.denoise(pc, cfg), {"FGBD_MASK_FOLD": "0"})
+    dev = denoise_frame(pc, cfg, device_ne=True)
+    host = fb.denoise(pc, cfg)
+    nofold = _in_thread(lambda: fb.denoise(pc, cfg), {"FGBD_MASK_FOLD": "0"})
+    assert nofold[1].selected_q == host[1].selected_q
+    assert nofold[1].masked_fraction == host[1].masked_fraction
+    assert np.max(np.abs(nofold[0].colors - host[0].colors)) <= 1e-9
     (a, ra), (b, rb) = dev, host
     assert ra.sigma_est == rb.sigma_est
     assert ra.device["eigenvalues"] == rb.device["eigenvalues"]
@@ -78,9 +84,9 @@ def test_device_finish_errors_match_host(gpu_ready):
                        [[10, 20, 30], [20, 30, 40], [30, 40, 50], [40, 50, 60]], 2)
     for cfg in (fb.FilterConfig(patch_size=7), fb.FilterConfig(patch_size=2)):
         errs = []
-        for env in (None, {"FGBD_MASK_FOLD": "0"}):
+        for dev_ne in (True, False):
             try:
-                _in_thread(lambda: fb.denoise(pc, cfg), env)
+                denoise_frame(pc, cfg, device_ne=dev_ne)
                 errs.append(None)
             except ValueError as e:
                 errs.append((type(e), str(e)))
