@@ -286,9 +286,6 @@ __device__ __forceinline__ void load_row_slots(const StepArgs& a, int64_t i, uin
 }
 
 // out = (d f + sum_s w_s f_s) / (2 d), the reference's order (filtering.py:132-155).
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 
 // out = (d f + acc) / (2 d) per channel (filtering.py:148-155); d = 0 keeps f
 __device__ __forceinline__ double4 finish_row(double d, const double4& f, double acc0,
@@ -389,37 +386,12 @@ __device__ __forceinline__ double4 row_w64(const StepArgs& a, const double4* in,
 
 // select_q bookkeeping after step q (filtering.py:244-255).  Pure function
 // of (state, crit): every block evaluates it identically.
-struct SelState {
-  int q, best_q, streak, stop, in_b, out_b, best_b;
-  double best_crit, prev;
-};
 
-__device__ __forceinline__ void select_update(SelState& s, double crit, int q_max,
-                                              int early_exit) {
-  s.q += 1;
-  if (crit < s.best_crit) {
-    s.best_crit = crit;
-    s.best_q = s.q;
-    s.best_b = s.out_b;
-  }
-  s.streak = crit > s.prev ? s.streak + 1 : 0;
-  s.prev = crit;
-  s.stop = (early_exit && s.streak >= 3) || (s.q >= q_max) || (s.best_crit == 0.0);
-  const int nin = s.out_b;
-  int nout = BUF_A;  // first of A, B, Y that is neither the new input nor the best
-  if (nout == nin || nout == s.best_b) nout = BUF_B;
-  if (nout == nin || nout == s.best_b) nout = BUF_Y;
-  s.in_b = nin;
-  s.out_b = nout;
-}
 
 __device__ __forceinline__ double4* pick_buf(const StepArgs& a, int b) {
   return b == 0 ? a.buf[0] : (b == 1 ? a.buf[1] : a.buf[2]);
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
 
 // One sweep of this block's rows: out = P in, optionally summing out^2 over
 // included rows.  The next row's graph slots are fetched while the current
@@ -553,37 +525,6 @@ constexpr int kWinRows = kTile + 2 * kHaloMax;
 constexpr int kStageBytes = kWinRows * 32 + 3 * kTile * 16;
 constexpr int kTmaSmem = 128 + 2 * kStageBytes;
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 
 struct TmaState {
   uint64_t* bar;        // [2]

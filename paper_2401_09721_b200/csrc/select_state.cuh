@@ -54,4 +54,29 @@ __device__ __forceinline__ void mask_finalize(Ctl* c, const double (&t)[7], int6
   c->early_exit = early_exit;
 }
 
+// select_q bookkeeping of one decided step (filtering.py:246-255)
+struct SelState {
+  int q, best_q, streak, stop, in_b, out_b, best_b;
+  double best_crit, prev;
+};
+
+__device__ __forceinline__ void select_update(SelState& s, double crit, int q_max,
+                                              int early_exit) {
+  s.q += 1;
+  if (crit < s.best_crit) {
+    s.best_crit = crit;
+    s.best_q = s.q;
+    s.best_b = s.out_b;
+  }
+  s.streak = crit > s.prev ? s.streak + 1 : 0;
+  s.prev = crit;
+  s.stop = (early_exit && s.streak >= 3) || (s.q >= q_max) || (s.best_crit == 0.0);
+  const int nin = s.out_b;
+  int nout = BUF_A;  // first of A, B, Y that is neither the new input nor the best
+  if (nout == nin || nout == s.best_b) nout = BUF_B;
+  if (nout == nin || nout == s.best_b) nout = BUF_Y;
+  s.in_b = nin;
+  s.out_b = nout;
+}
+
 }  // namespace fgbd

@@ -46,6 +46,8 @@
 #include "fgbd_internal.cuh"
 #include "select_state.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace fgbd {
 
 constexpr int kVec = 256;  // doubles per rank per all-gather stage
@@ -177,6 +179,8 @@ struct SlabGroup {  // one logical rank of this launch
   Ctl* ctl;
 };
 
+constexpr int kSlabMaxBlocks = 592;  // cooperative grid cap (148 SMs x 4)
+
 struct SlabArgs {
   int world;   // P
   int rank0;   // global rank of this launch's first group
@@ -186,8 +190,8 @@ struct SlabArgs {
   double4* bufs[kMaxRanks][3];           // every rank's Y/A/B by GLOBAL row (base - lo[r])
   double* slots[kMaxRanks];              // every rank's [2][P][4] criterion slots
   unsigned long long* flags[kMaxRanks];  // every rank's [P] step ticks
-  unsigned int* gbar;                    // local [groups][2] group-barrier counters
-  double* part;                          // local [groups][bpg][4] block partials
+  unsigned long long* release;           // local: "every rank finished step c" for this launch
+  double* part;                          // local [2][pstride] block partials (k_lf_run layout)
   SlabGroup grp[kMaxRanks];
   unsigned long long epoch;  // frame epoch: step ticks are epoch << 32 | step
   int fixed_steps;           // cached path when > 0 (no criterion)
@@ -202,37 +206,44 @@ __device__ __forceinline__ int owner_of(const SlabArgs& a, int64_t j) {
   return r;
 }
 
-struct SlabState {
-  int q, best_q, streak, stop, in_b, best_b;
-  double best_crit, prev;
-};
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-// Like k_lf_run (csrc/filter.cu): a row's three 16-byte graph loads land by
-// cp.async in this thread's own shared-memory slots one sweep iteration
-// ahead, and the graph row two iterations ahead is prefetched into L2, so
-// the sweep holds no graph registers and runs 3 blocks per SM.
+// The q scan of the slab ranks (filtering.py:225-256), built like k_lf_run
+// (csrc/filter.cu): a cooperative persistent launch, graph rows landed by
+// cp.async one sweep iteration ahead, the select_q decision lagged one step
+// and taken from block partials bulk-copied into shared memory during the
+// next sweep, one grid barrier per step.  Own rows are addressed by global
+// row; a foreign neighbour is read from its owner's buffer.
+//
+// When this launch holds every rank (one GPU; the emulation) the grid
+// barrier is the global barrier and the partials of all blocks are the
+// global total.  When the ranks span GPUs, after each grid barrier block 0
+// reduces the rank's partials, stores the total into slot r of every rank,
+// publishes the step tick and waits for every rank's tick (so every halo row
+// of the step is written and every rank's total has landed), then releases
+// this GPU's blocks; the lagged decision then sums the P slots in rank order.
 __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
+  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) int4 s_ell[];  // [2 stages][3 pairs][kBlock]
   __shared__ double s_red[32 * 3];
-  __shared__ SlabState s_st;
+  __shared__ __align__(16) double s_part[3 * kSlabMaxBlocks + 2];
+  __shared__ __align__(8) uint64_t s_pbar;
+  __shared__ SelState s_st;
   __shared__ double s_sy[3], s_sv2;
   __shared__ long long s_inc;
   __shared__ int s_qmax, s_mode, s_early, s_mask_all;
-  __shared__ bool s_last;
-  __shared__ unsigned int s_gen;
   const int g = blockIdx.x / a.bpg, lb = blockIdx.x % a.bpg;
   const int r = a.rank0 + g;
-  const int P = a.world;
+  const int P = a.world, nb = gridDim.x;
+  const bool local = a.groups == a.world;  // every rank in this launch
+  const bool bulk = a.select && local;
+  const int pstride = (3 * nb + 1) & ~1;
+  uint32_t pbar_uses = 0;
   const SlabGroup G = a.grp[g];
   Ctl* ctl = G.ctl;
   if (threadIdx.x == 0) {
+    if (bulk) mbar_init(&s_pbar, 1);
     if (a.select) {
-      s_st = SlabState{ctl->q, ctl->best_q, ctl->streak, ctl->stop, ctl->in_buf, ctl->best_buf,
-                       ctl->best_crit, ctl->prev_crit};
+      s_st = SelState{ctl->q, ctl->best_q, ctl->streak, ctl->stop, ctl->in_buf, ctl->out_buf,
+                      ctl->best_buf, ctl->best_crit, ctl->prev_crit};
       for (int k = 0; k < 3; ++k) s_sy[k] = ctl->sy[k];
       s_sv2 = ctl->sv2;
       s_inc = ctl->included;
@@ -241,7 +252,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
       s_early = ctl->early_exit;
       s_mask_all = ctl->mask_all;
     } else {
-      s_st = SlabState{0, 0, 0, a.fixed_steps <= 0, BUF_Y, BUF_Y, 0.0, 0.0};
+      s_st = SelState{0, 0, 0, a.fixed_steps <= 0, BUF_Y, BUF_A, BUF_Y, 0.0, 0.0};
       s_qmax = a.fixed_steps;
       s_mask_all = 1;
     }
@@ -250,21 +261,33 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
   const int64_t lo = a.lo[r], n_own = G.n_own;
   const int64_t chunk = ((n_own + a.bpg - 1) / a.bpg + blockDim.x - 1) / blockDim.x * blockDim.x;
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
-  unsigned int* gbar = a.gbar + 2 * g;
+  int c = s_st.q;  // x_c complete and decided (c = 0 at entry)
+  bool decided = true;
+  auto decide = [&](const double (&t)[3]) {
+    const double crit = criterion(s_sy, t, s_inc, s_sv2, s_mode);
+    s_st.out_b = s_st.in_b;  // x_c's buffer becomes the best if crit_c improves
+    s_st.q = c - 1;
+    select_update(s_st, crit, s_qmax, s_early);
+    if (lb == 0 && c < FGBD_TRACE_MAX) ctl->trace[c] = crit;
+  };
   while (!s_st.stop) {
-    const int ib = s_st.in_b, bb = s_st.best_b, q = s_st.q;
+    if (bulk && !decided && threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)(pstride * 8);
+      fence_proxy_async_global();  // the partials were stored before the barrier
+      mbar_expect_tx(&s_pbar, bytes);
+      bulk_g2s(s_part, a.part + (c & 1) * pstride, bytes, &s_pbar, policy_evict_last());
+    }
+    const int ib = s_st.in_b, bb = s_st.best_b;
     int ob = BUF_A;
     if (ob == ib || ob == bb) ob = BUF_B;
     if (ob == ib || ob == bb) ob = BUF_Y;
-    double4* out = a.bufs[r][ob];
-    double sx[3] = {0.0, 0.0, 0.0};
-    {
-      // this block's contiguous share of the rank's rows, next row's slots
-      // prefetched; gathers are branch-free (padding = own row, w = 0) and
-      // only rows outside [lo, hi) look up their owner's (peer) buffer
+    if (c < s_qmax) {
+      double sx[3] = {0.0, 0.0, 0.0};
       const double4* own_in = a.bufs[r][ib];
-      // own (local) rows: a contiguous share, or grid-stride waves when the
-      // signals do not fit in L2 (see fgbd::lf_contiguous)
+      double4* out = a.bufs[r][ob];
+      const bool mask_all = s_mask_all != 0;
+      // own (local) rows: a contiguous share, or grid-stride waves over the
+      // group when the signals do not fit in L2 (see fgbd::lf_contiguous)
       int64_t i = a.contiguous ? (int64_t)lb * chunk + threadIdx.x
                                : (int64_t)lb * blockDim.x + threadIdx.x;
       const int64_t end = a.contiguous ? min(n_own, (int64_t)(lb + 1) * chunk) : n_own;
@@ -277,7 +300,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
           for (int s = 0; s < kSlots; s += 2)
             asm volatile(
                 "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
-                    smem_addr(s_ell + (st * 3 + (s >> 1)) * T + threadIdx.x)),
+                    smem_u32(s_ell + (st * 3 + (s >> 1)) * T + threadIdx.x)),
                 "l"(G.E.nbr + eslot(s, n_own, row)), "l"(pol_stream)
                 : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -287,27 +310,26 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
         const int64_t inext = i + rstep;
         issue(inext, stage ^ 1);
         asm volatile("cp.async.wait_group 1;" ::: "memory");
-        int nb[kSlots];
+        int nbs[kSlots];
         float w[kSlots];
 #pragma unroll
         for (int s = 0; s < kSlots; s += 2) {
           const int4 pr = s_ell[(stage * 3 + (s >> 1)) * T + threadIdx.x];
-          nb[s] = pr.x;  // GLOBAL row | below-flag (bit 31)
+          nbs[s] = pr.x;  // GLOBAL row | below-flag (bit 31)
           w[s] = __int_as_float(pr.y);
-          nb[s + 1] = pr.z;
+          nbs[s + 1] = pr.z;
           w[s + 1] = __int_as_float(pr.w);
         }
         stage ^= 1;
         if (i + 2 * rstep < end)
 #pragma unroll
-          for (int s = 0; s < kSlots; s += 2)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(G.E.nbr + eslot(s, n_own, i + 2 * rstep)));
+          for (int s = 0; s < kSlots; s += 2) prefetch_l2(G.E.nbr + eslot(s, n_own, i + 2 * rstep));
         const int64_t gi = lo + i;
         const double4 f = ld_row_hint(own_in + gi, pol_keep);
         double4 gv[kSlots];
 #pragma unroll
         for (int s = 0; s < kSlots; ++s) {
-          const int64_t j = ell_j(nb[s]);
+          const int64_t j = ell_j(nbs[s]);
           FGBD_DCHECK(j >= 0 && j < a.lo[P]);
           const double4* src = own_in;
           if (__builtin_expect((uint64_t)(j - lo) >= (uint64_t)n_own, 0))
@@ -319,7 +341,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
         for (int s = 0; s < kSlots; ++s) {
           // (sum over original j > i) + (sum over j < i); padding adds +0.0
           const double ws = (double)w[s];
-          const bool below = ell_below(nb[s]);
+          const bool below = ell_below(nbs[s]);
           dlo = __dadd_rn(dlo, below ? ws : 0.0);
           dhi = __dadd_rn(dhi, below ? 0.0 : ws);
           acc0 = __dadd_rn(acc0, __dmul_rn(ws, gv[s].x));
@@ -335,7 +357,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
                            __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
         }
         st_row_hint(out + gi, o, pol_keep);
-        if (a.select && (s_mask_all || ((G.mask[i >> 5] >> (i & 31)) & 1u))) {
+        if (a.select && (mask_all || ((G.mask[i >> 5] >> (i & 31)) & 1u))) {
           sx[0] = fma(o.x, o.x, sx[0]);
           sx[1] = fma(o.y, o.y, sx[1]);
           sx[2] = fma(o.z, o.z, sx[2]);
@@ -343,85 +365,75 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
         i = inext;
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
-    }
-    block_sum<3>(sx, s_red);
-    double* part = a.part + ((int64_t)g * a.bpg + lb) * 4;
-    if (threadIdx.x == 0)
-      for (int k = 0; k < 3; ++k) part[k] = sx[k];
-    // Arrive.  The group's LAST block to arrive reduces the rank's partials
-    // (strided over its threads, then the fixed block tree), stores the total
-    // into every rank's slot, publishes the step tick, waits for every
-    // rank's tick and releases the group: one group-wide sync per step.
-    const int par = (q + 1) & 1;
-    const unsigned long long tick = (a.epoch << 32) | (unsigned long long)(q + 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned int gen0 = *(volatile unsigned int*)(gbar + 1);
-      __threadfence();
-      s_last = atomicAdd(gbar, 1u) == (unsigned)a.bpg - 1;
-      s_gen = gen0;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      double t[3] = {0.0, 0.0, 0.0};
-      for (int b = threadIdx.x; b < a.bpg; b += blockDim.x)
-        for (int k = 0; k < 3; ++k) t[k] += ld_cg(a.part + ((int64_t)g * a.bpg + b) * 4 + k);
-      block_sum<3>(t, s_red);
-      if (threadIdx.x == 0) {
-        for (int p = 0; p < P; ++p)
-          for (int k = 0; k < 3; ++k) a.slots[p][(par * P + r) * 4 + k] = t[k];
-        __threadfence_system();
-        for (int p = 0; p < P; ++p) st_release_sys(a.flags[p] + r, tick);
-        const long long t0 = clock64();
-        for (int p = 0; p < P; ++p)
-          while (ld_acquire_sys(a.flags[r] + p) < tick) {
-            if (clock64() - t0 > (1ll << 35)) {  // a peer died: report, do not hang
-              atomicOr(&ctl->err_flags, 4);
-              break;
-            }
-          }
-        atomicExch(gbar, 0u);  // every block of the group has arrived
-        __threadfence();
-        atomicAdd(gbar + 1, 1u);  // release
-      }
-    } else if (threadIdx.x == 0) {
-      const long long t0 = clock64();
-      while (*(volatile unsigned int*)(gbar + 1) == s_gen) {
-        if (clock64() - t0 > (1ll << 35)) {  // ~17 s: never hang the GPU; report it
-          atomicOr(&ctl->err_flags, 4);
-          break;
-        }
-      }
-      __threadfence();
-    }
-    __syncthreads();  // every rank's rows and totals of step q+1 are visible
-    if (threadIdx.x == 0) {
       if (a.select) {
-        double tot[3] = {0.0, 0.0, 0.0};
-        for (int p = 0; p < P; ++p)
-          for (int k = 0; k < 3; ++k) tot[k] += ld_cg(a.slots[r] + (par * P + p) * 4 + k);
-        const double crit = criterion(s_sy, tot, s_inc, s_sv2, s_mode);
-        SlabState& s = s_st;
-        s.q += 1;
-        if (crit < s.best_crit) {
-          s.best_crit = crit;
-          s.best_q = s.q;
-          s.best_b = ob;
-        }
-        s.streak = crit > s.prev ? s.streak + 1 : 0;
-        s.prev = crit;
-        s.stop = (s_early && s.streak >= 3) || (s.q >= s_qmax) || (s.best_crit == 0.0);
-        s.in_b = ob;
-        if (lb == 0 && s.q < FGBD_TRACE_MAX) ctl->trace[s.q] = crit;
-      } else {
-        s_st.q += 1;
-        s_st.stop = s_st.q >= s_qmax;
-        s_st.in_b = ob;
-        s_st.best_b = ob;
+        block_sum<3>(sx, s_red);
+        if (threadIdx.x == 0)
+          for (int k = 0; k < 3; ++k) a.part[((c + 1) & 1) * pstride + k * nb + blockIdx.x] = sx[k];
       }
     }
+    if (a.select && !decided) {
+      double t[3] = {0.0, 0.0, 0.0};
+      if (bulk) {  // every rank's blocks are in this launch: sum them all
+        mbar_wait(&s_pbar, pbar_uses & 1);
+        ++pbar_uses;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) t[k] += s_part[k * nb + b];
+        block_sum<3>(t, s_red);
+      } else if (threadIdx.x == 0) {  // the ranks' totals, in rank order
+        for (int p = 0; p < P; ++p)
+          for (int k = 0; k < 3; ++k) t[k] += ld_cg(a.slots[r] + ((c & 1) * P + p) * 4 + k);
+      }
+      if (threadIdx.x == 0) decide(t);
+      __syncthreads();
+    }
+    if (!a.select && c >= s_qmax) break;
+    if (s_st.stop) break;
+    grid.sync();  // this GPU's rows (and partials) of step c+1 are written
+    if (!local) {
+      const unsigned long long tick = (a.epoch << 32) | (unsigned long long)(c + 1);
+      if (blockIdx.x == 0) {
+        double t[3] = {0.0, 0.0, 0.0};
+        if (a.select) {
+          for (int b = threadIdx.x; b < nb; b += blockDim.x)
+            for (int k = 0; k < 3; ++k) t[k] += ld_cg(a.part + ((c + 1) & 1) * pstride + k * nb + b);
+          block_sum<3>(t, s_red);
+        }
+        if (threadIdx.x == 0) {
+          for (int p = 0; p < P; ++p)
+            for (int k = 0; k < 3; ++k) a.slots[p][(((c + 1) & 1) * P + r) * 4 + k] = t[k];
+          __threadfence_system();
+          for (int p = 0; p < P; ++p) st_release_sys(a.flags[p] + r, tick);
+          const long long t0 = clock64();
+          for (int p = 0; p < P; ++p)
+            while (ld_acquire_sys(a.flags[r] + p) < tick) {
+              if (clock64() - t0 > (1ll << 35)) {  // a peer died: report, do not hang
+                atomicOr(&ctl->err_flags, 4);
+                break;
+              }
+            }
+          st_release_sys(a.release, tick);
+        }
+      } else if (threadIdx.x == 0) {
+        const long long t0 = clock64();
+        while (ld_acquire_sys(a.release) < tick) {
+          if (clock64() - t0 > (1ll << 35)) {
+            atomicOr(&ctl->err_flags, 4);
+            break;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      s_st.in_b = ob;
+      s_st.out_b = ob;
+      s_st.q = c + 1;
+      if (!a.select) s_st.best_b = ob;
+    }
     __syncthreads();
+    c += 1;
+    decided = false;
   }
   if (lb == 0 && threadIdx.x == 0) {
     ctl->q = s_st.q;
@@ -537,8 +549,8 @@ struct fgbd_slab {
     void* ext = nullptr;        // ext_pc | ext_pos | ext_gidx | tile_cnt
     SlabGC g{};
   } loc[kMaxRanks];
-  unsigned int* gbar = nullptr;
-  double* part = nullptr;
+  unsigned long long* release = nullptr;  // k_lf_slab: "every rank finished the step"
+  double* part = nullptr;                 // k_lf_slab block partials [2][3 * blocks]
   int bpg_cap = 0;
   unsigned long long epoch = 1;
   cudaEvent_t rev[kMaxRanks][10] = {};  // per local rank: start/end of its phases
@@ -802,7 +814,7 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
       fgbd_ctx* c = s->loc[g].ctx;
       a.grp[g] = SlabGroup{EllRef{c->nbr, c->pay}, s->loc[g].g.n_own, c->mask, c->ctl};
     }
-    a.gbar = s->gbar;
+    a.release = s->release;
     a.part = s->part;
     a.epoch = s->epoch;
     a.select = cached_q < 0;
@@ -819,8 +831,6 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
     int64_t rows_here = 0;  // signal rows resident on this GPU
     for (int g = 0; g < s->groups; ++g) rows_here += s->loc[g].g.n_own;
     a.contiguous = lf_contiguous(parent, rows_here) ? 1 : 0;
-    FGBD_CUDA(parent,
-              cudaMemsetAsync(s->gbar, 0, 2 * s->groups * sizeof(unsigned), parent->stream));
     void* args[] = {&a};
     FGBD_CUDA(parent, cudaLaunchCooperativeKernel((void*)k_lf_slab, s->groups * a.bpg, kBlock,
                                                   args, smem, parent->stream));
@@ -980,9 +990,9 @@ fgbd_slab* fgbd_slab_create(fgbd_ctx* ctx, int32_t world, int32_t rank, int64_t 
         return fail();
       }
   s->bpg_cap = ctx->num_sms * 4;
-  if (cudaMalloc(&s->gbar, 2 * kMaxRanks * sizeof(unsigned)) != cudaSuccess ||
-      cudaMemset(s->gbar, 0, 2 * kMaxRanks * sizeof(unsigned)) != cudaSuccess ||
-      cudaMalloc(&s->part, (size_t)s->bpg_cap * 4 * sizeof(double)) != cudaSuccess) {
+  if (cudaMalloc(&s->release, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemset(s->release, 0, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&s->part, (size_t)2 * (3 * kSlabMaxBlocks + 2) * sizeof(double)) != cudaSuccess) {
     set_error(ctx, FGBD_E_CUDA, "slab scratch allocation failed");
     return fail();
   }
@@ -1007,7 +1017,7 @@ void fgbd_slab_destroy(fgbd_ctx* ctx, fgbd_slab* s) {
       fgbd_ctx_destroy(lc.ctx);
     }
   }
-  if (s->gbar) cudaFree(s->gbar);
+  if (s->release) cudaFree(s->release);
   if (s->part) cudaFree(s->part);
   for (auto& row : s->rev)
     for (auto& e : row)
