@@ -291,6 +291,8 @@ int32_t fgbd_select_tail(const double* lam, int32_t d, int32_t tau_divisor,
  * fgbd_slab_import before its first fgbd_denoise_slab. */
 #define FGBD_SLAB_EMULATED     0x1u
 #define FGBD_SLAB_FULL_OUTPUT  0x2u  /* multi-GPU: every rank receives the full frame */
+#define FGBD_SLAB_EXCHANGE     0x4u  /* emulated: run the filter's per-step cross-rank
+                                        exchange (slots + ticks) of the P-GPU protocol */
 typedef struct fgbd_slab fgbd_slab;
 fgbd_slab* fgbd_slab_create(fgbd_ctx* ctx, int32_t world, int32_t rank, int64_t n_total,
                             int64_t max_own, uint32_t slab_flags);

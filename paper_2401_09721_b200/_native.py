@@ -26,6 +26,7 @@ FLAG_WEIGHTS_F64 = 0x2
 FLAG_NO_TIMING = 0x4
 SLAB_EMULATED = 0x1
 SLAB_FULL_OUTPUT = 0x2
+SLAB_EXCHANGE = 0x4
 FLAG_REUSE_GRAPH = 0x8
 FLAG_STATIC_GEOMETRY = 0x10
 FLAG_DEVICE_NE = 0x20

@@ -197,6 +197,8 @@ struct SlabArgs {
   int fixed_steps;           // cached path when > 0 (no criterion)
   int select;
   int contiguous;            // rows per block: contiguous range (1) or grid-stride waves (0)
+  int exchange;              // per-step rank totals + ticks through peer memory (ranks span
+                             // GPUs; forced on one GPU to test the protocol)
 };
 
 __device__ __forceinline__ int owner_of(const SlabArgs& a, int64_t j) {
@@ -215,11 +217,12 @@ __device__ __forceinline__ int owner_of(const SlabArgs& a, int64_t j) {
 //
 // When this launch holds every rank (one GPU; the emulation) the grid
 // barrier is the global barrier and the partials of all blocks are the
-// global total.  When the ranks span GPUs, after each grid barrier block 0
-// reduces the rank's partials, stores the total into slot r of every rank,
-// publishes the step tick and waits for every rank's tick (so every halo row
-// of the step is written and every rank's total has landed), then releases
-// this GPU's blocks; the lagged decision then sums the P slots in rank order.
+// global total.  When the ranks span GPUs (`exchange`), after each grid
+// barrier the first block of each rank's group reduces the rank's partials,
+// stores the total into slot r of every rank, publishes the step tick and
+// waits for every rank's tick (so every halo row of the step is written and
+// every rank's total has landed), then releases this GPU's blocks; the
+// lagged decision then sums the P slots in rank order.
 __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) int4 s_ell[];  // [2 stages][3 pairs][kBlock]
@@ -233,8 +236,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
   const int g = blockIdx.x / a.bpg, lb = blockIdx.x % a.bpg;
   const int r = a.rank0 + g;
   const int P = a.world, nb = gridDim.x;
-  const bool local = a.groups == a.world;  // every rank in this launch
-  const bool bulk = a.select && local;
+  const bool exchange = a.exchange != 0;
+  const bool bulk = a.select && !exchange;  // every rank's blocks are in this launch
   const int pstride = (3 * nb + 1) & ~1;
   uint32_t pbar_uses = 0;
   const SlabGroup G = a.grp[g];
@@ -390,13 +393,14 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
     if (!a.select && c >= s_qmax) break;
     if (s_st.stop) break;
     grid.sync();  // this GPU's rows (and partials) of step c+1 are written
-    if (!local) {
+    if (exchange) {
       const unsigned long long tick = (a.epoch << 32) | (unsigned long long)(c + 1);
-      if (blockIdx.x == 0) {
+      if (lb == 0) {
         double t[3] = {0.0, 0.0, 0.0};
         if (a.select) {
-          for (int b = threadIdx.x; b < nb; b += blockDim.x)
-            for (int k = 0; k < 3; ++k) t[k] += ld_cg(a.part + ((c + 1) & 1) * pstride + k * nb + b);
+          for (int b = threadIdx.x; b < a.bpg; b += blockDim.x)
+            for (int k = 0; k < 3; ++k)
+              t[k] += ld_cg(a.part + ((c + 1) & 1) * pstride + k * nb + g * a.bpg + b);
           block_sum<3>(t, s_red);
         }
         if (threadIdx.x == 0) {
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_lf_slab(SlabArgs a) {
                 break;
               }
             }
-          st_release_sys(a.release, tick);
+          st_release_sys(a.release, tick);  // (every group's leader writes the same tick)
         }
       } else if (threadIdx.x == 0) {
         const long long t0 = clock64();
@@ -549,6 +553,7 @@ struct fgbd_slab {
     void* ext = nullptr;        // ext_pc | ext_pos | ext_gidx | tile_cnt
     SlabGC g{};
   } loc[kMaxRanks];
+  int force_exchange = 0;                 // FGBD_SLAB_EXCHANGE: the P-GPU protocol on one GPU
   unsigned long long* release = nullptr;  // k_lf_slab: "every rank finished the step"
   double* part = nullptr;                 // k_lf_slab block partials [2][3 * blocks]
   int bpg_cap = 0;
@@ -816,6 +821,7 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
     }
     a.release = s->release;
     a.part = s->part;
+    a.exchange = (s->groups != P || s->force_exchange) ? 1 : 0;
     a.epoch = s->epoch;
     a.select = cached_q < 0;
     a.fixed_steps = cached_q < 0 ? 0 : cached_q;
@@ -953,6 +959,7 @@ fgbd_slab* fgbd_slab_create(fgbd_ctx* ctx, int32_t world, int32_t rank, int64_t 
   s->rank = emulated ? 0 : rank;
   s->emulated = emulated;
   s->full = (flags & FGBD_SLAB_FULL_OUTPUT) && !emulated;
+  s->force_exchange = (flags & FGBD_SLAB_EXCHANGE) != 0;
   s->n_total = n_total;
   s->cap_rows = ((max_own + 65535) / 65536) * 65536;
   s->blk_cap = s->cap_rows + 1;

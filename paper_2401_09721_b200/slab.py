@@ -163,11 +163,14 @@ def _slab_for(ctx, world, rank, n_total, max_own, flags, pg):
 def denoise_slab(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
                  cached_q: int | None = None, cached_sigma_est: float | None = None, *,
                  process_group=None, emulate_ranks: int | None = None,
-                 output: str = "full", partition: SlabPartition | None = None):
+                 output: str = "full", partition: SlabPartition | None = None,
+                 emulate_exchange: bool = False):
     """`denoise` with the frame split into z-slabs over P ranks.
 
     Returns (PointCloud, DenoiseReport) like `denoise`; with output="local"
     (multi-GPU only) returns (own global indices, own colours, report).
+    `emulate_exchange` runs the filter's per-step cross-rank exchange of the
+    P-GPU protocol in the emulation too (testing).
     """
     n = pc_noisy.n_points
     if n < 2:
@@ -197,6 +200,8 @@ def denoise_slab(pc_noisy: PointCloud, cfg: FilterConfig = FilterConfig(),
         raise ValueError(f"partition is for {part.world} ranks, not {world}")
     ctx = nat.context()
     flags = nat.SLAB_EMULATED if emulated else (nat.SLAB_FULL_OUTPUT if output == "full" else 0)
+    if emulated and emulate_exchange:
+        flags |= nat.SLAB_EXCHANGE
     max_own = int(part.counts.max())
     slab = _slab_for(ctx, world, rank, n, max_own, flags, process_group)
     coords, colors = pc_noisy.coords, pc_noisy.colors

@@ -57,11 +57,11 @@ def test_denoise_8m_matches_reference(gpu_ready, frame):
     _check(rec, clean, out, rep)
 
 
-@pytest.mark.parametrize("ranks", [2, 4, 8])
-def test_denoise_slab_8m_matches_reference(gpu_ready, frame, ranks):
+@pytest.mark.parametrize("ranks,exchange", [(2, False), (4, False), (8, False), (8, True)])
+def test_denoise_slab_8m_matches_reference(gpu_ready, frame, ranks, exchange):
     from paper_2401_09721_b200.slab import denoise_slab
 
     rec, clean, noisy, out, rep = frame
-    b, rb = denoise_slab(noisy, emulate_ranks=ranks)
+    b, rb = denoise_slab(noisy, emulate_ranks=ranks, emulate_exchange=exchange)
     _check(rec, clean, b, rb)
     assert np.array_equal(b.colors, out.colors)

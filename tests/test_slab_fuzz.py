@@ -54,7 +54,9 @@ def test_slab_matches_denoise(gpu_ready, seed):
         with pytest.raises(type(e)):
             denoise_slab(pc, cfg, emulate_ranks=ranks)
         return
-    b, rb = denoise_slab(pc, cfg, emulate_ranks=ranks)
+    # odd seeds run the filter's per-step cross-rank exchange (the P-GPU
+    # protocol: rank totals in peer slots, release/acquire ticks)
+    b, rb = denoise_slab(pc, cfg, emulate_ranks=ranks, emulate_exchange=bool(seed & 1))
     assert rb.selected_q == ra.selected_q
     assert rb.device["steps"] == ra.device["steps"]
     assert rb.device["sigma_g"] == ra.device["sigma_g"]
@@ -66,7 +68,7 @@ def test_slab_matches_denoise(gpu_ready, seed):
     # the cached path with the selected q
     c, _ = fb.denoise(pc, cfg, cached_q=ra.selected_q, cached_sigma_est=ra.sigma_est)
     d, _ = denoise_slab(pc, cfg, cached_q=ra.selected_q, cached_sigma_est=ra.sigma_est,
-                        emulate_ranks=ranks)
+                        emulate_ranks=ranks, emulate_exchange=bool(seed & 1))
     assert np.array_equal(c.colors, d.colors)
 
 
