@@ -128,3 +128,21 @@ def test_sequence_static_geometry(gpu_ready):
     for f in range(7):
         assert np.array_equal(a[f][0].colors, b[f][0].colors)
         assert a[f][1].selected_q == b[f][1].selected_q
+
+
+@pytest.mark.parametrize("n", [131_075, 1_000_003])
+def test_pageable_and_pinned_inputs_agree(gpu_ready, n):
+    """Pageable arrays go through the context's chunked pinned staging
+    (csrc/hoststage.cu, 2 MB chunks, ragged last chunk); pinned arrays copy
+    directly.  Same frame, same bits."""
+    from paper_2401_09721_b200 import _native as nat
+
+    clean, _ = fb.generate_cloud("two-tone", n, seed=3)
+    noisy = fb.add_gaussian_noise(clean, 12.0, seed=4)
+    pg = fb.PointCloud(np.array(noisy.coords), np.array(noisy.colors), noisy.bit_depth)
+    c = nat.pinned_empty(noisy.coords.shape, np.int64)
+    c[...] = noisy.coords
+    y = nat.pinned_empty(noisy.colors.shape, np.float64)
+    y[...] = noisy.colors
+    pn = fb.PointCloud(c, y, noisy.bit_depth)
+    same(fb.denoise(pg), fb.denoise(pn))
