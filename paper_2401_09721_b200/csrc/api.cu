@@ -349,6 +349,16 @@ cudaEvent_t& device_last_compute(int device) {
   return ev[device & 63];
 }
 
+// Far-gather filter variant (k_lf_run FAR): on when at least half of the
+// graph's slots point more than kFarRows rows away -- random clouds, whose
+// scattered gathers only evict reusable rows from L1 (-8% filter time
+// there, +7% on lattices; profiles/r2_summary.md).  FGBD_LF_FAR overrides.
+int far_choice(const fgbd_ctx* ctx, const Ctl& h) {
+  if (ctx->lf_far >= 0) return ctx->lf_far > 0;
+  const unsigned long long nnz = 2 * h.n_edges;
+  return nnz > 0 && 2 * h.far_slots >= nnz;
+}
+
 double ev_sec(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
@@ -457,6 +467,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_SORT_DERIVED")) ctx->sort_derived = std::atoi(v);
   if (const char* v = std::getenv("FGBD_ROWS_GRID")) ctx->rows_grid = std::atoi(v);
   if (const char* v = std::getenv("FGBD_MASK_FOLD")) ctx->mask_fold = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_LF_FAR")) ctx->lf_far = std::atoi(v);
   if (const char* v = std::getenv("FGBD_HOST_THREADS")) ctx->host_threads = std::max(0, std::atoi(v));
   if (ensure_capacity(ctx, max_points > 0 ? max_points : 1, 0) != FGBD_OK) {
     set_error(nullptr, FGBD_E_CUDA, ctx->err);
@@ -624,6 +635,8 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   std::memset(&nz, 0, sizeof(nz));
   bool folded = false;     // the FSLR mask folded into the first filter step
   bool device_ne = false;  // NE finished on the device (FGBD_FLAG_DEVICE_NE)
+  // the filter's far-gather variant: known here only for a reused graph
+  ctx->lf_far_now = reuse ? ctx->held_far : (ctx->lf_far > 0);
   if (cached_q >= 0) {
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
     int fin = BUF_Y;
@@ -656,6 +669,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   } else if (cached_q < 0) {
     const int D = cfg->patch_size;
     if ((rc = pull_ctl(ctx))) return rc;
+    ctx->lf_far_now = far_choice(ctx, *ctx->ctl_host);
     if ((rc = check_graph_ctl(ctx, bits))) return rc;
     const int maxdeg = ctx->ctl_host->max_deg;
     if (D > 1 + maxdeg)
@@ -694,6 +708,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   if (cached_q < 0 && device_ne && (rc = collect_noise(ctx, cfg->patch_size, &nz))) return rc;
   const Ctl& h = *ctx->ctl_host;
   if (want_reuse && !reuse) {  // the copy now describes a complete graph with weights
+    ctx->held_far = far_choice(ctx, h);
     ctx->held_edges = h.n_edges;
     ctx->held_sigma_g = h.sigma_g;
     ctx->held_max_deg = h.max_deg;

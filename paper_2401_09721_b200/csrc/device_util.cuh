@@ -162,6 +162,26 @@ __device__ __forceinline__ double4 ld_row_hint(const double4* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return v;
 }
+#ifndef FGBD_LF_FARMODE
+#define FGBD_LF_FARMODE 0  // far gathers: 0 ld.global.cg, 1 L1::no_allocate, 2 L1::evict_first
+#endif
+__device__ __forceinline__ double4 ld_row_cg_hint(const double4* p, uint64_t pol) {
+  double4 v;
+#if FGBD_LF_FARMODE == 1
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p), "l"(pol));
+#elif FGBD_LF_FARMODE == 2
+  asm volatile("ld.global.L1::evict_first.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p), "l"(pol));
+#else
+  asm volatile("ld.global.cg.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+               : "l"(p), "l"(pol));
+#endif
+  return v;
+}
 __device__ __forceinline__ void st_row_hint(double4* p, double4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v.x),
                "d"(v.y), "d"(v.z), "d"(v.w), "l"(pol)

@@ -46,6 +46,7 @@ constexpr int kSortTile = kSortThreads * kSortIPT;  // keys per onesweep tile
 constexpr int kRadix = 256;
 constexpr int kMaxPasses = 8;
 constexpr int kSlots = 6;              // max SLG degree: 2 neighbours x 3 lines
+constexpr int kFarRows = 512;          // a "far" neighbour row (scattered gather) for the filter
 
 enum BufId { BUF_Y = 0, BUF_A = 1, BUF_B = 2 };
 
@@ -93,6 +94,7 @@ struct Ctl {
   int nz_m[3], nz_fb[3], nz_direct[3];
   double fslr_thr;              // 2 sigma_est
   int fslr_active;              // FSLR mask on
+  unsigned long long far_slots; // k_rows: edges to rows more than kFarRows away (both ends)
 };
 
 enum NzErr {
@@ -186,7 +188,10 @@ struct fgbd_ctx {
   int reorder_rows = 1;         // FGBD_REORDER: denoise-path rows in scan-line-1 order
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
   int sort_derived = 1;         // FGBD_SORT_DERIVED: lines 2/3 by one field of the previous order
-  int mask_fold = 1;            // FGBD_MASK_FOLD: the FSLR mask built by the first filter step
+  int mask_fold = 1;
+  int lf_far = -1;              // FGBD_LF_FAR: far gathers skip L1 (-1 auto: >= half the slots far)
+  int lf_far_now = 0;           // the choice for the frame being filtered
+  int held_far = 0;             // far-slot majority of the held (reused) graph            // FGBD_MASK_FOLD: the FSLR mask built by the first filter step
   int rows_grid = 0;            // FGBD_ROWS_GRID: k_rows grid, 0 = 8 blocks/SM (grid-stride), 1 = one row per thread
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)

@@ -307,6 +307,7 @@ __device__ __forceinline__ double4 finish_row(double d, const double4& f, double
                       __ddiv_rn(__dadd_rn(__dmul_rn(d, f.z), acc2), d2), 0.0);
 }
 
+template <int FAR = 0>
 __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const float (&wf)[kSlots],
                                                   const double4* in, int64_t i, uint64_t pol_keep,
                                                   double4* f_out = nullptr) {
@@ -321,6 +322,13 @@ __device__ __forceinline__ double4 row_from_slots(const int (&nb)[kSlots], const
   // per-slot branches.
 #pragma unroll
   for (int s = 0; s < kSlots; ++s)
+  if (FAR > 0) {
+    // far neighbours (scattered gathers on random clouds) bypass L1, so
+    // they do not evict the rows the block re-reads (own rows, near ones)
+    const int64_t dj = (int64_t)ell_j(nb[s]) - i;
+    g[s] = (dj > FAR || dj < -FAR) ? ld_row_cg_hint(in + ell_j(nb[s]), pol_keep)
+                                   : ld_row_hint(in + ell_j(nb[s]), pol_keep);
+  } else
 #if FGBD_LF_SIGHINT
     g[s] = ld_row_hint(in + ell_j(nb[s]), pol_keep);
 #else
@@ -399,7 +407,7 @@ __device__ __forceinline__ double4* pick_buf(const StepArgs& a, int b) {
 // FGBD_LF_ELLSMEM by cp.async into this thread's shared-memory slots, which
 // frees 12 registers), and the graph row FGBD_LF_PFD iterations ahead is
 // prefetched into L2.
-template <int WM, bool SUMS, bool FOLD = false>
+template <int WM, bool SUMS, bool FOLD = false, int FAR = 0>
 __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, double4* out,
                                       bool mask_all, float neg_inv_sg2, double (&sx)[3],
                                       int4* s_ell, double* xs = nullptr /*[10] with FOLD*/,
@@ -475,7 +483,7 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
       for (int s = 0; s < kSlots; s += 2)
         prefetch_l2(a.E.nbr + eslot(s, n, i + FGBD_LF_PFD * stride));
     double4 f;
-    const double4 o = row_from_slots(nbc, wc, in, i, pol_keep, FOLD ? &f : nullptr);
+    const double4 o = row_from_slots<FAR>(nbc, wc, in, i, pol_keep, FOLD ? &f : nullptr);
     st_row_hint(out + i, o, pol_keep);
     if (FOLD) {
       // k_mask's work for this row (filtering.py:175-194, 237-243): the
@@ -726,7 +734,7 @@ __device__ __forceinline__ void grid_wait(unsigned int* bar, unsigned int old) {
 }
 
 template <int WM, bool SELECT, int BLK = kBlock, int MINB = 3, bool TMA = false,
-          bool P2P = false>
+          bool P2P = false, int FAR = 0>
 __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char dyn_smem[];
@@ -842,13 +850,14 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       } else if (SELECT && !P2P && a.fold && c == 0) {
         // step 1 also does k_mask's work (FSLR bits + the initial totals)
         double xs[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-        sweep<WM, SELECT, true>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx,
-                                s_ell, xs, s_thr, s_active);
+        sweep<WM, SELECT, true, FAR>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2,
+                                     sx, s_ell, xs, s_thr, s_active);
         block_sum<10>(xs, s_red10);
         if (threadIdx.x == 0)
           for (int k = 0; k < 10; ++k) a.xpart[k * nb + blockIdx.x] = xs[k];
       } else {
-        sweep<WM, SELECT>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2, sx, s_ell);
+        sweep<WM, SELECT, false, FAR>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2,
+                                      sx, s_ell);
       }
 #if FGBD_LF_TLOG
       if ((threadIdx.x & 31) == 0 && c < kTlogSteps && (threadIdx.x >> 5) < 16)
@@ -1207,9 +1216,10 @@ bool fgbd::lf_contiguous(const fgbd_ctx* ctx, int64_t rows) {
 
 namespace fgbd {
 
-template <int WM, bool SELECT, int BLK, int MINB, bool TMA = false, bool P2P = false>
+template <int WM, bool SELECT, int BLK, int MINB, bool TMA = false, bool P2P = false,
+          int FAR = 0>
 static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
-  auto kern = k_lf_run<WM, SELECT, BLK, MINB, TMA, P2P>;
+  auto kern = k_lf_run<WM, SELECT, BLK, MINB, TMA, P2P, FAR>;
   constexpr int kEllSmem = (FGBD_LF_ELLSMEM && WM == W_STORED) ? (FGBD_LF_ELLSMEM + 1) * 3 * BLK * 16 : 0;
   const int smem = TMA ? kTmaSmem : kEllSmem;
   if (ctx->coop_blocks[slot] == 0) {
@@ -1269,6 +1279,9 @@ static int launch_run_any(fgbd_ctx* ctx, StepArgs& a) {
     return launch_run_k<W_STORED, SELECT, kTile, 3, true>(ctx, a, 40 + (SELECT ? 1 : 0));
   if (ctx->lf_variant == 13)  // neighbourhood flags instead of the grid barrier
     return launch_run_k<W_STORED, SELECT, kBlock, 3, false, true>(ctx, a, 42 + (SELECT ? 1 : 0));
+  if (ctx->lf_far_now && ctx->lf_shape == 0)  // mostly scattered gathers: far ones skip L1
+    return launch_run_k<W_STORED, SELECT, kBlock, 3, false, false, kFarRows>(ctx, a,
+                                                                             44 + (SELECT ? 1 : 0));
   return launch_run<W_STORED, SELECT>(ctx, a);
 }
 
@@ -1306,6 +1319,8 @@ int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, int q_max, int mode, in
   a.q_max = q_max;
   a.mode = mode;
   a.early_exit = early_exit;
+  if (ctx->lf_far_now && ctx->lf_shape == 0)
+    return launch_run_k<W_STORED, true, kBlock, 3, false, false, kFarRows>(ctx, a, 45);
   return launch_run<W_STORED, true>(ctx, a);
 }
 

@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
   __shared__ unsigned long long s_red[32 * 2];
   __shared__ bool s_last;
   u128 sg_sum = 0;  // exact: the same bits for any partition of the edges
-  unsigned long long e_cnt = 0;
+  unsigned long long e_cnt = 0, far = 0;
   int maxdeg = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // rows differ from points only when the line-1 order is not the identity
@@ -595,9 +595,22 @@ __global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
     }
     meta[r] = (uint32_t)deg | (order << 3);
     maxdeg = max(maxdeg, deg);
+    const int64_t own = SLAB ? sl.lo + r : r;
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      if (s < deg) {
+        const int64_t d = (int64_t)ell_j(word[s]) - own;
+        far += (d > kFarRows || d < -kFarRows);
+      }
   }
   // block reduce (sum, count) and the max degree
   maxdeg = __reduce_max_sync(kFull, maxdeg);
+  {
+    unsigned long long f = far;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(kFull, f, o);
+    if ((threadIdx.x & 31) == 0 && f) atomicAdd(&ctl->far_slots, f);
+  }
   if ((threadIdx.x & 31) == 0 && maxdeg > 0) atomicMax(&ctl->max_deg, maxdeg);
   unsigned long long* up = reinterpret_cast<unsigned long long*>(partials);
   const u128 bs = block_sum_u128(sg_sum, s_red);
