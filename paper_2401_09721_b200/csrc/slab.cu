@@ -557,7 +557,7 @@ struct fgbd_slab {
   unsigned long long* release = nullptr;  // k_lf_slab: "every rank finished the step"
   double* part = nullptr;                 // k_lf_slab block partials [2][3 * blocks]
   int bpg_cap = 0;
-  unsigned long long epoch = 1;
+  unsigned long long epoch = 1;  // frame counter (incremented at the start of each frame)
   cudaEvent_t rev[kMaxRanks][10] = {};  // per local rank: start/end of its phases
 };
 
@@ -674,6 +674,10 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
   cudaEvent_t* ev = parent->ev;
   std::lock_guard<std::mutex> lock(slab_device_mutex(parent->device));
   NvtxRange nv_frame("fgbd.denoise_slab");
+  // a fresh epoch per call, taken before anything can fail: a frame that
+  // stops early never leaves ticks the next frame could mistake for its own
+  // (every rank makes the same calls, so the epochs agree)
+  s->epoch += 1;
   if (timing) FGBD_CUDA(parent, cudaEventRecord(ev[0], parent->stream));
   // ---- phase 1: upload own points, sort, block lists, own Y ------------------
   int64_t off = 0;
@@ -875,7 +879,6 @@ int slab_frame(fgbd_ctx* parent, fgbd_slab* s, const int64_t* coords, const doub
                                       (size_t)s->n_total * 24, cudaMemcpyDefault, parent->stream));
   }
   if (timing) FGBD_CUDA(parent, cudaEventRecord(ev[4], parent->stream));
-  s->epoch += 1;
   for (int g = 0; g < s->groups; ++g)
     if (int rc = pull(s->loc[g].ctx)) return set_error(parent, rc, s->loc[g].ctx->err);
   if (timing) FGBD_CUDA(parent, cudaEventRecord(ev[5], parent->stream));
