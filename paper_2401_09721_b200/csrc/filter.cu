@@ -411,7 +411,7 @@ template <int WM, bool SUMS, bool FOLD = false, int FAR = 0>
 __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, double4* out,
                                       bool mask_all, float neg_inv_sg2, double (&sx)[3],
                                       int4* s_ell, double* xs = nullptr /*[10] with FOLD*/,
-                                      double thr = 0.0, int active = 0) {
+                                      const double* thr_p = nullptr, const int* active_p = nullptr) {
   const int64_t n = a.n;
   // rows of this block: a contiguous range walked in blockDim strides (the
   // neighbours of raster / scan-ordered clouds then mostly hit this SM's L1),
@@ -488,7 +488,9 @@ __device__ __forceinline__ void sweep(const StepArgs& a, const double4* in, doub
     if (FOLD) {
       // k_mask's work for this row (filtering.py:175-194, 237-243): the
       // FSLR bit, and the initial totals over included / all rows
-      const bool inc = !(active && a.fslr[i] > thr);
+      // (the threshold is read from shared memory here, not held in a
+      // register across the kernel: that cost the hot loop a spill)
+      const bool inc = !(*active_p && a.fslr[i] > *thr_p);
       const unsigned bits = __ballot_sync(__activemask(), inc);
       if ((threadIdx.x & 31) == 0) const_cast<uint32_t*>(a.mask)[i >> 5] = bits;
       const double y2[3] = {f.x * f.x, f.y * f.y, f.z * f.z};
@@ -851,7 +853,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
         // step 1 also does k_mask's work (FSLR bits + the initial totals)
         double xs[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         sweep<WM, SELECT, true, FAR>(a, pick_buf(a, ib), pick_buf(a, ob), mask_all, neg_inv_sg2,
-                                     sx, s_ell, xs, s_thr, s_active);
+                                     sx, s_ell, xs, &s_thr, &s_active);
         block_sum<10>(xs, s_red10);
         if (threadIdx.x == 0)
           for (int k = 0; k < 10; ++k) a.xpart[k * nb + blockIdx.x] = xs[k];
