@@ -20,7 +20,7 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libfgbd_b200.so"
-SOURCES = ["graph.cu", "noise.cu", "filter.cu", "stage.cu", "slab.cu", "ply.cu", "knn.cu", "measure.cu", "noisegen.cu", "hoststage.cu", "api.cu"]
+SOURCES = ["graph.cu", "noise.cu", "filter.cu", "stage.cu", "slab.cu", "ply.cu", "knn.cu", "measure.cu", "noisegen.cu", "hoststage.cu", "slg.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]

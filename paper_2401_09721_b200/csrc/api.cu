@@ -465,6 +465,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_LF_HALO")) ctx->lf_halo = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("FGBD_SORT_DERIVED")) ctx->sort_derived = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_SLG_COOP")) ctx->slg_coop = std::atoi(v);
   if (const char* v = std::getenv("FGBD_ROWS_GRID")) ctx->rows_grid = std::atoi(v);
   if (const char* v = std::getenv("FGBD_MASK_FOLD")) ctx->mask_fold = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_FAR")) ctx->lf_far = std::atoi(v);
@@ -487,6 +488,7 @@ void fgbd_ctx_destroy(fgbd_ctx* ctx) {
   if (ctx->partials) cudaFree(ctx->partials);
   if (ctx->sort.hist) cudaFree(ctx->sort.hist);
   if (ctx->sort.tile_ctr) cudaFree(ctx->sort.tile_ctr);
+  if (ctx->slg_cnt) cudaFree(ctx->slg_cnt);
   if (ctx->d_bufs) cudaFree(ctx->d_bufs);
   if (ctx->tickets) cudaFree(ctx->tickets);
   if (ctx->csr_scratch) cudaFree(ctx->csr_scratch);

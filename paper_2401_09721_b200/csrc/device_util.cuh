@@ -310,6 +310,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Grid barrier of a cooperative launch over a zero-initialised word that
+// only this launch uses: one release atomic per block (block 0 adds
+// 2^31 - (blocks - 1), so the top bit flips exactly when the last block
+// arrives), a RELAXED spin, then one acquire fence.  cooperative_groups'
+// grid.sync() spins with acquire loads, i.e. an L1 invalidation (CCTL.IVALL)
+// per poll, which keeps wiping the L1 of the blocks on the same SM that are
+// still working; here each block invalidates once, on leaving.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+    unsigned int old, cur;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
+    do {
+      asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+    } while (((cur ^ old) & 0x80000000u) == 0);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }

@@ -188,10 +188,13 @@ struct fgbd_ctx {
   int reorder_rows = 1;         // FGBD_REORDER: denoise-path rows in scan-line-1 order
   int prep_mult = 8;            // k_prep blocks per SM (FGBD_PREP_MULT)
   int sort_derived = 1;         // FGBD_SORT_DERIVED: lines 2/3 by one field of the previous order
-  int mask_fold = 1;
+  int mask_fold = 1;             // FGBD_MASK_FOLD: the FSLR mask built by the first filter step
   int lf_far = -1;              // FGBD_LF_FAR: far gathers skip L1 (-1 auto: >= half the slots far)
   int lf_far_now = 0;           // the choice for the frame being filtered
-  int held_far = 0;             // far-slot majority of the held (reused) graph            // FGBD_MASK_FOLD: the FSLR mask built by the first filter step
+  int held_far = 0;             // far-slot majority of the held (reused) graph
+  int slg_coop = 1;             // FGBD_SLG_COOP: scan-line front end in one cooperative launch
+  int slg_grid[2] = {0, 0};     // its co-resident grid (32- / 64-bit codes)
+  uint32_t* slg_cnt = nullptr;  // its digit-count table
   int rows_grid = 0;            // FGBD_ROWS_GRID: k_rows grid, 0 = 8 blocks/SM (grid-stride), 1 = one row per thread
   int l2_persist = 0;           // pin the ELL graph in L2 (FGBD_L2_PERSIST)
   int ne_variant = 1;           // 0: warp per channel, 1: thread per point (FGBD_NE_VARIANT)
@@ -293,6 +296,8 @@ int ensure_w64(fgbd_ctx* ctx, int64_t n);
 // reorder: store rows in scan-line-1 order (ctx->rowid / ctx->pos) -- the
 // denoise path; stage-API graphs keep rows in point order
 int launch_graph(fgbd_ctx* ctx, int64_t n, int bits, bool reorder = false);
+// slg.cu: codes + scan-line orders + rank neighbours in one cooperative launch
+int launch_slg(fgbd_ctx* ctx, int64_t n, int b, int* pos, int64_t row_base);
 // Converts the ell payload (squared distances) into Gaussian weights.
 int launch_weights(fgbd_ctx* ctx, int64_t n, int bits, int w64);
 // Stand-alone stable argsort of 64-bit keys (radix_argsort).

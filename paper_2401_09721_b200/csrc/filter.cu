@@ -55,6 +55,11 @@
 // 0: cooperative_groups grid.sync() after the decision)
 #define FGBD_LF_SPLITBAR 0
 #endif
+// the per-step grid barrier: 1 grid_barrier (relaxed spin, one L1
+// invalidation per block), 0 cooperative_groups grid.sync()
+#ifndef FGBD_LF_BAR
+#define FGBD_LF_BAR 0
+#endif
 #ifndef FGBD_LF_ELLSMEM
 // graph slots of the next FGBD_LF_ELLSMEM rows via cp.async into shared memory (0: registers;
 // profiles/r1_summary.md r1c: 1 stage -2.5% filter time, 2 / 3 stages slower -- less L1)
@@ -967,7 +972,11 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       grid_wait(a.gbar, gen0);
     } else {
       TLOG(c, 2);
+#if FGBD_LF_BAR
+      grid_barrier(a.gbar);
+#else
       grid.sync();
+#endif
     }
     if (threadIdx.x == 0) {
       s_st.in_b = ob;

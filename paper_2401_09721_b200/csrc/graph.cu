@@ -897,14 +897,20 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
 
 template <typename K>
 static int graph_impl(fgbd_ctx* ctx, int64_t n, int b, bool reorder) {
-  const int passes = (3 * b + 7) / 8;
-  int rc = run_sort<K, true>(ctx, n, b, 3, passes, nullptr);
-  if (rc) return rc;
-  // rows in scan-line-1 order: row k holds the point of line-1 rank k
-  ctx->rowid = reorder ? ctx->perm[0] : nullptr;
-  if (reorder) FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_perm, ctx->stream));
   int* pos = reorder ? ctx->pos : nullptr;
-  {
+  if (ctx->slg_coop) {
+    // codes, the three orders and the rank neighbours in one launch (slg.cu)
+    int rc = launch_slg(ctx, n, b, pos, 0);
+    if (rc) return rc;
+    ctx->rowid = reorder ? ctx->perm[0] : nullptr;
+    if (reorder) FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_perm, ctx->stream));
+  } else {
+    const int passes = (3 * b + 7) / 8;
+    int rc = run_sort<K, true>(ctx, n, b, 3, passes, nullptr);
+    if (rc) return rc;
+    // rows in scan-line-1 order: row k holds the point of line-1 rank k
+    ctx->rowid = reorder ? ctx->perm[0] : nullptr;
+    if (reorder) FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_perm, ctx->stream));
     dim3 grid(grid_for(n, 1 << 20), 3);
     k_neighbors<<<grid, kBlock, 0, ctx->stream>>>(ctx->perm[0], ctx->perm[1], ctx->perm[2], n,
                                                   ctx->cand, pos, ctx->ctl);
@@ -1300,16 +1306,19 @@ template <typename K>
 static int slab_own_impl(fgbd_ctx* ctx, SlabGC& g) {
   const int64_t n = g.n_own;
   const int b = g.b;
-  const int passes = (3 * b + 7) / 8;
-  int rc = run_sort<K, true>(ctx, n, b, 3, passes, nullptr);
-  if (rc) return rc;
-  ctx->rowid = ctx->perm[0];
-  {
+  if (ctx->slg_coop) {
+    int rc = launch_slg(ctx, n, b, g.ext_pos, g.lo);
+    if (rc) return rc;
+  } else {
+    const int passes = (3 * b + 7) / 8;
+    int rc = run_sort<K, true>(ctx, n, b, 3, passes, nullptr);
+    if (rc) return rc;
     dim3 grid(grid_for(n, 1 << 20), 3);
     k_neighbors<<<grid, kBlock, 0, ctx->stream>>>(ctx->perm[0], ctx->perm[1], ctx->perm[2], n,
                                                   ctx->cand, g.ext_pos, ctx->ctl, g.lo);
     FGBD_LAUNCH(ctx);
   }
+  ctx->rowid = ctx->perm[0];
   // own packed coordinates into the extended array (halo records follow them)
   FGBD_CUDA(ctx, cudaMemcpyAsync(g.ext_pc, ctx->pc, (size_t)n * sizeof(K), cudaMemcpyDeviceToDevice,
                                  ctx->stream));
