@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kNeThreads) k_noise(const uint32_t* __restrict
 // the ELL payload (exact squared length) into the fp32 Gaussian weight --
 // the rows are being read here anyway, so Eq. (4) costs no extra pass.
 constexpr int kNe2Warps = 4;
+constexpr int kWTab = 64;  // weights tabulated for squared lengths below this
 
 __device__ __forceinline__ double ch(const double4& v, int c) {
   return c == 0 ? v.x : (c == 1 ? v.y : v.z);
@@ -190,6 +191,14 @@ __global__ void __launch_bounds__(kNe2Warps * 32, FGBD_NE_MINB) k_noise2(const u
     sg_rcp = rcp_ok(sg2);
     if (sg_rcp) rsg2 = __drcp_rn(sg2);
   }
+  // Eq. (4) for the small squared lengths (lattice neighbours): the same
+  // expression once per block instead of an fp64 exp per slot
+  __shared__ float s_wtab[kWTab];
+  if (WEIGHTS) {
+    for (int t = threadIdx.x; t < kWTab; t += blockDim.x)
+      s_wtab[t] = (float)exp(sg_rcp ? div_rcp(-(double)t, sg2, rsg2) : __ddiv_rn(-(double)t, sg2));
+    __syncthreads();
+  }
   const double rD = __drcp_rn((double)D), r3 = __drcp_rn(3.0);
   const int64_t nchunks = (n + 31) / 32;
   const int64_t wstride = (int64_t)gridDim.x * kNe2Warps;
@@ -206,20 +215,23 @@ __global__ void __launch_bounds__(kNe2Warps * 32, FGBD_NE_MINB) k_noise2(const u
     for (int r = 0; r < 7; ++r) v[r] = make_double4(0, 0, 0, 0);
     if (valid) {
       mt = meta[i];
+      // the three slot pairs in flight together (the weight stores below
+      // would otherwise order each load after the previous pair's store)
+      int4 prs[kSlots / 2];
+#pragma unroll
+      for (int s = 0; s < kSlots; s += 2) prs[s / 2] = *reinterpret_cast<const int4*>(ell.nbr + eslot(s, n, i));
 #pragma unroll
       for (int s = 0; s < kSlots; s += 2) {
-        int4 pr = *reinterpret_cast<const int4*>(ell.nbr + eslot(s, n, i));
+        int4 pr = prs[s / 2];
         nb[s] = ell_j(pr.x);
         nb[s + 1] = ell_j(pr.z);
         if (WEIGHTS) {
-          const double q0 = sg_rcp ? div_rcp(-(double)(uint32_t)pr.y, sg2, rsg2)
-                                   : __ddiv_rn(-(double)(uint32_t)pr.y, sg2);
-          const double q1 = sg_rcp ? div_rcp(-(double)(uint32_t)pr.w, sg2, rsg2)
-                                   : __ddiv_rn(-(double)(uint32_t)pr.w, sg2);
-          const double w0 = nb[s] != (int)gi ? exp(q0) : 0.0;
-          const double w1 = nb[s + 1] != (int)gi ? exp(q1) : 0.0;
-          pr.y = __float_as_int((float)w0);
-          pr.w = __float_as_int((float)w1);
+          auto weight = [&](uint32_t sq) -> float {
+            if (sq < (uint32_t)kWTab) return s_wtab[sq];
+            return (float)exp(sg_rcp ? div_rcp(-(double)sq, sg2, rsg2) : __ddiv_rn(-(double)sq, sg2));
+          };
+          pr.y = __float_as_int(nb[s] != (int)gi ? weight((uint32_t)pr.y) : 0.0f);
+          pr.w = __float_as_int(nb[s + 1] != (int)gi ? weight((uint32_t)pr.w) : 0.0f);
           *reinterpret_cast<int4*>(ell.nbr + eslot(s, n, i)) = pr;
         }
       }
