@@ -333,6 +333,8 @@ int launch_finish_noise(fgbd_ctx* ctx, int patch, int divisor, int fslr_enabled,
 int collect_noise(fgbd_ctx* ctx, int patch, fgbd_noise* out);
 int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err,
                        int* direct_off);
+int jacobi_eigenvalues_multi(int nm, const double* const* s, int d, double* const* out_desc,
+                             std::string* err, int* rc, int* direct_off);
 int select_tail_host(const double* lam, int d, int divisor, int* m, double* tau,
                      int* fallback, std::string* err);
 

@@ -445,8 +445,11 @@ struct RowsSlab {
   int64_t lo;            // global row of own row 0
 };
 
+#ifndef FGBD_ROWS_MINB
+#define FGBD_ROWS_MINB 4  // 64 registers, 4 blocks per SM: k_rows 55 -> 46 us (1M ramp, r2bi)
+#endif
 template <typename K, bool BIG, bool SLAB = false>
-__global__ void __launch_bounds__(kBlock) k_rows(const int2* __restrict__ cand,
+__global__ void __launch_bounds__(kBlock, FGBD_ROWS_MINB) k_rows(const int2* __restrict__ cand,
                                                  const K* __restrict__ pc, int64_t n, int b,
                                                  const int* __restrict__ pos,
                                                  const uint32_t* __restrict__ rowid, EllRef ell,

@@ -368,33 +368,51 @@ static double np_pairwise_sum(const double* x, int n) {
   return res;
 }
 
-int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err,
-                       int* direct_off) {
-  if (direct_off) *direct_off = 0;
-  // symmetry check on the raw input (noise.py:142-144)
-  double scale = 0.0, asym = 0.0;
-  for (int i = 0; i < d * d; ++i) scale = std::max(scale, std::fabs(s[i]));
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j) asym = std::max(asym, std::fabs(s[i * d + j] - s[j * d + i]));
-  if (scale > 0 && asym > 1e-9 * scale) {
-    *err = "matrix is not symmetric within tolerance";
-    return FGBD_E_NOISE;
+namespace {
+
+// One matrix's cyclic Jacobi (noise.py:133-185), as resumable steps so that
+// jacobi_eigenvalues_multi can run the three channels in lockstep.
+struct Jacobi {
+  int d = 0;
+  std::vector<double> a, cp, cq, sq;
+  double target = 0.0;
+  double* out = nullptr;
+  int state = 0;  // 0 rotating, 1 finished, 2 failed
+  int rc = FGBD_OK;
+  int direct_off = 0;
+  std::string err;
+
+  void finish() {
+    for (int i = 0; i < d; ++i) out[i] = a[i * d + i];
+    std::sort(out, out + d, [](double x, double y) { return x > y; });
+    state = 1;
   }
-  std::vector<double> a(d * d);
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j) a[i * d + j] = (s[i * d + j] + s[j * d + i]) * 0.5;
-  auto finish = [&]() {
-    for (int i = 0; i < d; ++i) out_desc[i] = a[i * d + i];
-    std::sort(out_desc, out_desc + d, [](double x, double y) { return x > y; });
-  };
-  double fro2 = 0.0;
-  for (int i = 0; i < d * d; ++i) fro2 += a[i] * a[i];
-  const double norm = std::sqrt(fro2);
-  if (norm == 0.0 || d == 1) {
-    finish();
-    return FGBD_OK;
+  void fail(int code, std::string msg) {
+    rc = code;
+    err = std::move(msg);
+    state = 2;
   }
-  const double target = 1e-12 * norm;
+  void init(const double* s, int d_, double* out_) {
+    d = d_;
+    out = out_;
+    // symmetry check on the raw input (noise.py:142-144)
+    double scale = 0.0, asym = 0.0;
+    for (int i = 0; i < d * d; ++i) scale = std::max(scale, std::fabs(s[i]));
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) asym = std::max(asym, std::fabs(s[i * d + j] - s[j * d + i]));
+    if (scale > 0 && asym > 1e-9 * scale) return fail(FGBD_E_NOISE, "matrix is not symmetric within tolerance");
+    a.resize(d * d);
+    cp.resize(d);
+    cq.resize(d);
+    sq.resize(d * d);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) a[i * d + j] = (s[i * d + j] + s[j * d + i]) * 0.5;
+    double fro2 = 0.0;
+    for (int i = 0; i < d * d; ++i) fro2 += a[i] * a[i];
+    const double norm = std::sqrt(fro2);
+    if (norm == 0.0 || d == 1) return finish();
+    target = 1e-12 * norm;
+  }
   // noise.py:152: sqrt(max(np.sum(a * a) - np.sum(np.diag(a) ** 2), 0)).  The
   // difference cancels catastrophically near convergence (|a|^2 ~ 1e7 leaves
   // an absolute error ~1e-9, i.e. off ~ 1e-4 >> the 1e-12 |a| target), so
@@ -402,77 +420,112 @@ int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* er
   // rounding of these two sums: reproduce numpy's order exactly -- pairwise
   // (8 strided accumulators) over the d*d products, sequential over the
   // diagonal (fewer than 8 terms).
-  auto off_norm = [&]() {
-    double sq[49];
+  double off_norm() {
     for (int i = 0; i < d * d; ++i) sq[i] = a[i] * a[i];
-    const double all = np_pairwise_sum(sq, d * d);
+    const double all = np_pairwise_sum(sq.data(), d * d);
     double dg = 0.0;
     for (int i = 0; i < d; ++i) dg += a[i * d + i] * a[i * d + i];
     return std::sqrt(std::max(all - dg, 0.0));
-  };
-  std::vector<double> cp(d), cq(d);
+  }
+  void rotate(int p, int q) {
+    const double apq = a[p * d + q];
+    if (apq == 0.0) return;
+    const double diff = a[q * d + q] - a[p * d + p];
+    double t;
+    if (std::fabs(apq) < 1e-36 * std::fabs(diff)) {
+      t = apq / diff;
+    } else {
+      const double theta = diff / (2.0 * apq);
+      t = np_sign(theta) / (std::fabs(theta) + std::hypot(theta, 1.0));
+      if (t == 0.0) t = 1.0;
+    }
+    const double c = 1.0 / std::sqrt(t * t + 1.0);
+    const double sn = t * c;
+    for (int i = 0; i < d; ++i) {
+      cp[i] = a[i * d + p];
+      cq[i] = a[i * d + q];
+    }
+    for (int i = 0; i < d; ++i) {
+      a[i * d + p] = c * cp[i] - sn * cq[i];
+      a[i * d + q] = sn * cp[i] + c * cq[i];
+    }
+    for (int j = 0; j < d; ++j) {
+      cp[j] = a[p * d + j];
+      cq[j] = a[q * d + j];
+    }
+    for (int j = 0; j < d; ++j) {
+      a[p * d + j] = c * cp[j] - sn * cq[j];
+      a[q * d + j] = sn * cp[j] + c * cq[j];
+    }
+    a[p * d + q] = 0.0;
+    a[q * d + p] = 0.0;
+  }
+  // after the last sweep
+  void final_check() {
+    const double off = off_norm();
+    // The difference-of-sums norm above has a floor of ~sqrt(ulp(|a|^2)): on
+    // some matrices the reference reports non-convergence (noise.py:179-185)
+    // while its off-diagonal entries are all exactly zero, and which matrices
+    // hit this depends on the last ulp of the covariance (i.e. on the BLAS
+    // build).  Only a matrix whose off-diagonal norm, summed directly, is
+    // still above the target is reported as a failure; see DESIGN.md "Parity".
+    double off_direct = 0.0;
+    for (int p = 0; p < d; ++p)
+      for (int q = 0; q < d; ++q)
+        if (p != q) off_direct += a[p * d + q] * a[p * d + q];
+    if (off <= target || std::sqrt(off_direct) <= target) {
+      // the reference would have raised here (noise.py:180-185): say so
+      if (!(off <= target)) direct_off = 1;
+      return finish();
+    }
+    char buf[128];
+    std::snprintf(buf, sizeof(buf), "Jacobi did not converge in 50 sweeps (off-diagonal %.3e)", off);
+    fail(FGBD_E_NOISE, buf);
+  }
+};
+
+}  // namespace
+
+// nm <= 3 matrices of one size in lockstep: each matrix's arithmetic is
+// exactly jacobi_eigenvalues', but the rotation chains of the channels --
+// divisions, hypot and square roots, ~100 dependent cycles each -- are
+// independent, so the CPU overlaps them (the host NE finish ran the three
+// channels one after the other).
+int jacobi_eigenvalues_multi(int nm, const double* const* s, int d, double* const* out_desc,
+                             std::string* err, int* rc, int* direct_off) {
+  Jacobi J[3];
+  nm = std::min(nm, 3);
+  for (int m = 0; m < nm; ++m) J[m].init(s[m], d, out_desc[m]);
   for (int sweep = 0; sweep < 50; ++sweep) {
-    if (off_norm() <= target) {
-      finish();
-      return FGBD_OK;
+    bool any = false;
+    for (int m = 0; m < nm; ++m) {
+      if (J[m].state != 0) continue;
+      if (J[m].off_norm() <= J[m].target) J[m].finish();
+      else any = true;
     }
-    for (int p = 0; p < d - 1; ++p) {
-      for (int q = p + 1; q < d; ++q) {
-        const double apq = a[p * d + q];
-        if (apq == 0.0) continue;
-        const double diff = a[q * d + q] - a[p * d + p];
-        double t;
-        if (std::fabs(apq) < 1e-36 * std::fabs(diff)) {
-          t = apq / diff;
-        } else {
-          const double theta = diff / (2.0 * apq);
-          t = np_sign(theta) / (std::fabs(theta) + std::hypot(theta, 1.0));
-          if (t == 0.0) t = 1.0;
-        }
-        const double c = 1.0 / std::sqrt(t * t + 1.0);
-        const double sn = t * c;
-        for (int i = 0; i < d; ++i) {
-          cp[i] = a[i * d + p];
-          cq[i] = a[i * d + q];
-        }
-        for (int i = 0; i < d; ++i) {
-          a[i * d + p] = c * cp[i] - sn * cq[i];
-          a[i * d + q] = sn * cp[i] + c * cq[i];
-        }
-        for (int j = 0; j < d; ++j) {
-          cp[j] = a[p * d + j];
-          cq[j] = a[q * d + j];
-        }
-        for (int j = 0; j < d; ++j) {
-          a[p * d + j] = c * cp[j] - sn * cq[j];
-          a[q * d + j] = sn * cp[j] + c * cq[j];
-        }
-        a[p * d + q] = 0.0;
-        a[q * d + p] = 0.0;
-      }
-    }
+    if (!any) break;
+    for (int p = 0; p < d - 1; ++p)
+      for (int q = p + 1; q < d; ++q)
+        for (int m = 0; m < nm; ++m)
+          if (J[m].state == 0) J[m].rotate(p, q);
   }
-  const double off = off_norm();
-  // The difference-of-sums norm above has a floor of ~sqrt(ulp(|a|^2)): on
-  // some matrices the reference reports non-convergence (noise.py:179-185)
-  // while its off-diagonal entries are all exactly zero, and which matrices
-  // hit this depends on the last ulp of the covariance (i.e. on the BLAS
-  // build).  Only a matrix whose off-diagonal norm, summed directly, is still
-  // above the target is reported as a failure; see DESIGN.md "Parity".
-  double off_direct = 0.0;
-  for (int p = 0; p < d; ++p)
-    for (int q = 0; q < d; ++q)
-      if (p != q) off_direct += a[p * d + q] * a[p * d + q];
-  if (off <= target || std::sqrt(off_direct) <= target) {
-    // the reference would have raised here (noise.py:180-185): say so
-    if (direct_off && !(off <= target)) *direct_off = 1;
-    finish();
-    return FGBD_OK;
+  int first = FGBD_OK;
+  for (int m = 0; m < nm; ++m) {
+    if (J[m].state == 0) J[m].final_check();
+    rc[m] = J[m].rc;
+    if (err) err[m] = J[m].err;
+    if (direct_off) direct_off[m] = J[m].direct_off;
+    if (!first) first = J[m].rc;
   }
-  char buf[128];
-  std::snprintf(buf, sizeof(buf), "Jacobi did not converge in 50 sweeps (off-diagonal %.3e)", off);
-  *err = buf;
-  return FGBD_E_NOISE;
+  return first;
+}
+
+int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* err,
+                       int* direct_off) {
+  int rc = FGBD_OK, flag = 0;
+  jacobi_eigenvalues_multi(1, &s, d, &out_desc, err, &rc, &flag);
+  if (direct_off) *direct_off = flag;
+  return rc;
 }
 
 static double median_of(const double* v, int m) {
@@ -927,31 +980,41 @@ int finish_noise(fgbd_ctx* ctx, int D, int divisor, fgbd_noise* out) {
   if (ne < 2)
     return set_error(ctx, FGBD_E_NOISE, "need at least 2 patches, have " + std::to_string(ne));
   double sig[3];
+  double cov[3][7 * 7], lam[3][7];
   for (int c = 0; c < 3; ++c) {
     // Gram matrix of shifted patch rows: G[k][l] = sum (a_k-128)(a_l-128),
     // G[k][7] = sum (a_k-128), G[7][7] = eligible count
     const double* G = h.gram[c];
     double mu[7];
     for (int k = 0; k < D; ++k) mu[k] = G[k * 8 + 7] / (double)ne;
-    double cov[7 * 7];
     for (int k = 0; k < D; ++k) {
       for (int l = k; l < D; ++l) {
         const double v = G[k * 8 + l] / (double)ne - mu[k] * mu[l];
-        cov[k * D + l] = v;
-        cov[l * D + k] = v;
+        cov[c][k * D + l] = v;
+        cov[c][l * D + k] = v;
       }
     }
     for (int k = 0; k < D; ++k)
-      for (int l = 0; l < D; ++l) out->covariance[c][k][l] = cov[k * D + l];
+      for (int l = 0; l < D; ++l) out->covariance[c][k][l] = cov[c][k * D + l];
+  }
+  // the three channels' Jacobi in lockstep (bit-identical per channel);
+  // errors are then reported in channel order, as the reference raises them
+  std::string jerr[3];
+  int jrc[3];
+  {
+    const double* sm[3] = {cov[0], cov[1], cov[2]};
+    double* om[3] = {lam[0], lam[1], lam[2]};
+    jacobi_eigenvalues_multi(3, sm, D, om, jerr, jrc, out->jacobi_direct_off);
+  }
+  for (int c = 0; c < 3; ++c) {
     std::string err;
-    double lam[7];
-    int rc = jacobi_eigenvalues(cov, D, lam, &err, &out->jacobi_direct_off[c]);
-    if (rc) return set_error(ctx, rc, err);
+    if (jrc[c]) return set_error(ctx, jrc[c], jerr[c]);
+    int rc;
     int m, fb;
     double tau;
-    rc = select_tail_host(lam, D, divisor, &m, &tau, &fb, &err);
+    rc = select_tail_host(lam[c], D, divisor, &m, &tau, &fb, &err);
     if (rc) return set_error(ctx, rc, err);
-    for (int k = 0; k < D; ++k) out->eigenvalues[c][k] = lam[k];
+    for (int k = 0; k < D; ++k) out->eigenvalues[c][k] = lam[c][k];
     out->m[c] = m;
     out->tau[c] = tau;
     out->fallback[c] = fb;
