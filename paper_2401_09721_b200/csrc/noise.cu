@@ -349,23 +349,29 @@ int launch_noise_slab(fgbd_ctx* ctx, int64_t n, int patch, const SlabView& v) {
 
 static double np_sign(double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); }
 
-// numpy's add.reduce over a contiguous float64 vector of n <= 128 values
-// (pairwise_sum: n < 8 sequential from 0; else 8 strided accumulators,
-// combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail sequentially)
+// numpy's pairwise summation of a contiguous float64 array (pairwise_sum in
+// numpy/core/src/umath/loops_utils.h): a sequential loop below 8 terms, 8
+// strided accumulators up to 128, halves (rounded down to a multiple of 8)
+// above
 static double np_pairwise_sum(const double* x, int n) {
   if (n < 8) {
     double res = 0.0;
     for (int i = 0; i < n; ++i) res += x[i];
     return res;
   }
-  double r[8];
-  for (int j = 0; j < 8; ++j) r[j] = x[j];
-  int i = 8;
-  for (; i < n - (n % 8); i += 8)
-    for (int j = 0; j < 8; ++j) r[j] += x[i + j];
-  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-  for (; i < n; ++i) res += x[i];
-  return res;
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = x[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += x[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += x[i];
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise_sum(x, n2) + np_pairwise_sum(x + n2, n - n2);
 }
 
 namespace {
@@ -417,14 +423,13 @@ struct Jacobi {
   // difference cancels catastrophically near convergence (|a|^2 ~ 1e7 leaves
   // an absolute error ~1e-9, i.e. off ~ 1e-4 >> the 1e-12 |a| target), so
   // whether the reference converges or reports a failure is decided by the
-  // rounding of these two sums: reproduce numpy's order exactly -- pairwise
-  // (8 strided accumulators) over the d*d products, sequential over the
-  // diagonal (fewer than 8 terms).
+  // rounding of these two sums: reproduce numpy's order exactly -- its
+  // pairwise summation over the d*d products and over the d diagonal squares.
   double off_norm() {
     for (int i = 0; i < d * d; ++i) sq[i] = a[i] * a[i];
     const double all = np_pairwise_sum(sq.data(), d * d);
-    double dg = 0.0;
-    for (int i = 0; i < d; ++i) dg += a[i * d + i] * a[i * d + i];
+    for (int i = 0; i < d; ++i) sq[i] = a[i * d + i] * a[i * d + i];
+    const double dg = np_pairwise_sum(sq.data(), d);
     return std::sqrt(std::max(all - dg, 0.0));
   }
   void rotate(int p, int q) {

@@ -106,6 +106,25 @@ def test_host_jacobi_spec_examples():
         fb.select_tail(np.array([1.0, 0.5]))
 
 
+def test_host_jacobi_large_matrices_match_oracle(monkeypatch):
+    """The public symmetric_eigenvalues takes any square size (noise.py:133):
+    beyond 7x7 numpy's pairwise sums change shape (8 accumulators from 8
+    terms, recursive halves above 128) -- same eigenvalues bit for bit.
+    (Large matrices often end on the difference-of-sums floor: the oracle
+    then computes the documented direct-norm acceptance.)"""
+    import oracle.fgbd_oracle as O
+
+    monkeypatch.setattr(O, "JACOBI_DIRECT_OFF_FALLBACK", True)
+    rng = np.random.default_rng(11)
+    for d in (8, 9, 10, 12, 16, 20):
+        for _ in range(6):
+            a = rng.standard_normal((d, d)) * 30.0
+            s = a @ a.T / d + np.diag(rng.uniform(0, 5, d))
+            lam = fb.symmetric_eigenvalues(s)
+            ref = O.symmetric_eigenvalues(s)
+            assert np.array_equal(lam, ref), d
+
+
 def test_filter_config_validation_matches_reference():
     with pytest.raises(fb.FilterError, match="q_max must be >= 0"):
         fb.FilterConfig(q_max=-1)
