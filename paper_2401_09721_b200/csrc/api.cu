@@ -1,5 +1,6 @@
 // C ABI (include/fgbd_b200.h): context lifetime, the `denoise` drop-in
 // (reference filtering.py:259-328) and the stage entry points.
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -532,9 +533,34 @@ void fgbd_host_free(void* p) {
   if (p) cudaFreeHost(p);
 }
 
+// FGBD_HOST_TLOG=1 (diagnostic): host timestamps of fgbd_denoise's phases
+// printed to stderr, microseconds since entry
+namespace {
+struct HostTlog {
+  bool on = false;
+  std::chrono::steady_clock::time_point t0;
+  char buf[512];
+  int len = 0;
+  HostTlog() {
+    static const bool want = std::getenv("FGBD_HOST_TLOG") != nullptr;
+    on = want;
+    if (on) t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on || len > 440) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    len += std::snprintf(buf + len, sizeof(buf) - len, " %s=%.1f", what, us);
+  }
+  ~HostTlog() {
+    if (on) std::fprintf(stderr, "host tlog:%s\n", buf);
+  }
+};
+}  // namespace
+
 int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors, int64_t n,
                      int32_t bits, const fgbd_config* cfg, int32_t cached_q, double cached_sigma,
                      double* out_colors, fgbd_report* rep, uint32_t flags) {
+  HostTlog tl;
   if (!ctx || !rep) return set_error(ctx, FGBD_E_ARG, "null context or report");
   NvtxRange nv_frame("fgbd.denoise");
   cudaSetDevice(ctx->device);
@@ -564,6 +590,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   if ((rc = check_graph_input(ctx, n, bits))) return rc;
   cudaEvent_t* ev = ctx->ev;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[0], ctx->stream));
+  tl.mark("ev0");
   if ((rc = ensure_capacity(ctx, n, 3 * bits > 32))) return rc;
   apply_l2_policy(ctx, n);
   const int64_t* frame_coords = dev ? coords : ctx->coords64;
@@ -615,6 +642,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   if (cudaEvent_t prev = device_last_compute(ctx->device))
     FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, prev, 0));
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[1], ctx->stream));
+  tl.mark("ev1");
   // the NE pass converts the ELL payloads to weights itself when it can
   const bool fuse_w = !reuse && cached_q < 0 && !w64 && bits <= 15 && ctx->ne_variant == 1;
   if (reuse) {
@@ -629,6 +657,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   }
   rep->graph_reused = reuse ? 1 : 0;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
+  tl.mark("graph");
   // colours travel (and are re-laid out) while the graph is being built
   if ((rc = upload_colors_async(ctx, frame_colors, n, colors_dev))) return rc;
   FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_side, 0));
@@ -670,7 +699,9 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   } else if (cached_q < 0) {
     const int D = cfg->patch_size;
+    tl.mark("ne_launched");
     if ((rc = pull_ctl(ctx))) return rc;
+    tl.mark("ne_pulled");
     ctx->lf_far_now = far_choice(ctx, *ctx->ctl_host);
     if ((rc = check_graph_ctl(ctx, bits))) return rc;
     const int maxdeg = ctx->ctl_host->max_deg;
@@ -679,16 +710,19 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
                                               " exceeds 1 + max degree (" +
                                               std::to_string(1 + maxdeg) + ") of this graph");
     if ((rc = finish_noise(ctx, D, cfg->tau_divisor, &nz))) return rc;
+    tl.mark("ne_done");
     const double sig = nz.sigma_est;
     const int active = cfg->fslr_enabled && !(sig < cfg->fslr_sigma_floor);
     if (!folded && (rc = launch_mask(ctx, n, sig, active, cfg->q_max, cfg->criterion_mode,
                                      cfg->early_exit, nullptr)))
       return rc;
     if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[3], ctx->stream));
+    tl.mark("ev3");
     if (folded) {
       if ((rc = launch_select_steps_folded(ctx, n, cfg->q_max, cfg->criterion_mode,
                                            cfg->early_exit, &sig, active)))
         return rc;
+      tl.mark("lf_launched");
     } else if ((rc = launch_select_steps(ctx, n, cfg->q_max, w64))) {
       return rc;
     }
@@ -696,16 +730,42 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   }
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
+  // the frame's control block travels right behind its last kernel, so the
+  // one wait below (the lock's or the download's) also covers it
+  FGBD_CUDA(ctx, cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
   FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
   device_last_compute(ctx->device) = ctx->ev_done;
   // a frame with a host round trip inside keeps the lock until it is done
-  if (!ctx->async_lock || (cached_q < 0 && !device_ne))
-    FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_done));
+  const bool held = !ctx->async_lock || (cached_q < 0 && !device_ne);
+  // device outputs: nothing follows, so the frame's last event goes in now
+  // (recording it after the wait cost a submission round trip, ~10 us)
+  if (dev && timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
+  tl.mark("enqueued");
+  // Each elapsed-time query is a ~3.5 us driver call: a frame that waits
+  // here anyway reads the stage times while the filter still runs, so only
+  // the last one falls after the frame's end
+  bool stages_read = false;
+  auto read_stage_times = [&]() {
+    rep->t_h2d = ev_sec(ev[0], ev[1]);
+    rep->t_graph_construction = ev_sec(ev[1], ev[2]);
+    cudaEventSynchronize(ev[3]);
+    rep->t_noise_estimation = cached_q >= 0 ? 0.0 : ev_sec(ev[2], ev[3]);
+    cudaEventSynchronize(ev[6]);
+    rep->t_lf_steps = ev_sec(ev[3], ev[6]);
+    cudaEventSynchronize(ev[4]);
+    rep->t_low_pass_filter = ev_sec(ev[3], ev[4]);
+    stages_read = true;
+  };
+  if (held && timing) read_stage_times();
+  if (held) FGBD_CUDA(ctx, cudaEventSynchronize(dev && timing ? ev[5] : ctx->ev_done));
+  tl.mark("done");
   compute_lock.unlock();
   NvtxRange nv_out("fgbd.download");
   if (!dev && (rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), false))) return rc;
-  if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
-  if ((rc = pull_ctl(ctx))) return rc;
+  if (!dev && timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
+  if (!dev || !held) FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  tl.mark("synced");
   if ((rc = check_graph_ctl(ctx, bits))) return rc;
   if (cached_q < 0 && device_ne && (rc = collect_noise(ctx, cfg->patch_size, &nz))) return rc;
   const Ctl& h = *ctx->ctl_host;
@@ -740,16 +800,16 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     rep->n_trace = std::min(h.steps + 1, FGBD_TRACE_MAX);
     for (int k = 0; k < rep->n_trace; ++k) rep->trace[k] = h.trace[k];
   }
+  tl.mark("report");
   if (timing) {
-    rep->t_graph_construction = ev_sec(ev[1], ev[2]);
-    rep->t_noise_estimation = cached_q >= 0 ? 0.0 : ev_sec(ev[2], ev[3]);
-    rep->t_low_pass_filter = ev_sec(ev[3], ev[4]);
-    rep->t_total = ev_sec(ev[0], ev[5]);
-    rep->t_lf_steps = ev_sec(ev[3], ev[6]);
-    rep->t_h2d = ev_sec(ev[0], ev[1]);
+    if (!stages_read) read_stage_times();
     rep->t_d2h = ev_sec(ev[4], ev[5]);
+    // the chain ev0 .. ev5, summed (one driver query fewer)
+    rep->t_total = rep->t_h2d + rep->t_graph_construction + rep->t_noise_estimation +
+                   rep->t_low_pass_filter + rep->t_d2h;
   }
   rep->gpu_launches = ctx->launches;
+  tl.mark("exit");
   return FGBD_OK;
 }
 

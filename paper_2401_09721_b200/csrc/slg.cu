@@ -379,10 +379,10 @@ static int slg_grid(fgbd_ctx* ctx, size_t smem) {
 template <typename K>
 static int slg_impl(fgbd_ctx* ctx, int64_t n, int b, int* pos, int64_t row_base) {
   const size_t smem = (size_t)(kSlgWarps * kSlgMaxR + kSlgMaxGrid) * sizeof(uint32_t);
-  FGBD_CUDA(ctx, cudaFuncSetAttribute(k_slg<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
   int& G = ctx->slg_grid[sizeof(K) == 8];
-  if (G <= 0) {
+  if (G <= 0) {  // once per context: attribute + co-resident grid
+    FGBD_CUDA(ctx, cudaFuncSetAttribute(k_slg<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
     G = slg_grid<K>(ctx, smem);
     if (G <= 0) return set_error(ctx, FGBD_E_CUDA, "scan-line kernel cannot be co-resident");
   }
