@@ -467,6 +467,8 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("FGBD_SORT_DERIVED")) ctx->sort_derived = std::atoi(v);
   if (const char* v = std::getenv("FGBD_SLG_COOP")) ctx->slg_coop = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_LF_HOLD")) ctx->lf_hold = std::atoi(v);
+  if (ctx->lf_hold >= 0) ctx->hold_guess = ctx->lf_hold;
   if (const char* v = std::getenv("FGBD_ROWS_GRID")) ctx->rows_grid = std::atoi(v);
   if (const char* v = std::getenv("FGBD_MASK_FOLD")) ctx->mask_fold = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_FAR")) ctx->lf_far = std::atoi(v);
@@ -730,12 +732,15 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   }
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[4], ctx->stream));
-  // the frame's control block travels right behind its last kernel, so the
-  // one wait below (the lock's or the download's) also covers it
-  FGBD_CUDA(ctx, cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
   FGBD_CUDA(ctx, cudaEventRecord(ctx->ev_done, ctx->stream));
   device_last_compute(ctx->device) = ctx->ev_done;
+  // the frame's control block travels right behind its last kernel, so the
+  // one wait below (the lock's or the download's) also covers it -- but
+  // after ev_done: the next frame's kernels wait for ev_done, and a copy in
+  // front of it queued them behind this frame's output download (r2f3:
+  // 300-frame video 721 -> 609 frames/s)
+  FGBD_CUDA(ctx, cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
   // a frame with a host round trip inside keeps the lock until it is done
   const bool held = !ctx->async_lock || (cached_q < 0 && !device_ne);
   // device outputs: nothing follows, so the frame's last event goes in now
@@ -758,7 +763,12 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     stages_read = true;
   };
   if (held && timing) read_stage_times();
-  if (held) FGBD_CUDA(ctx, cudaEventSynchronize(dev && timing ? ev[5] : ctx->ev_done));
+  if (held) {
+    // device outputs: the wait covers the control block too
+    if (dev && timing) FGBD_CUDA(ctx, cudaEventSynchronize(ev[5]));
+    else if (dev) FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    else FGBD_CUDA(ctx, cudaEventSynchronize(ctx->ev_done));
+  }
   tl.mark("done");
   compute_lock.unlock();
   NvtxRange nv_out("fgbd.download");
@@ -789,6 +799,9 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   } else {
     rep->selected_q = h.best_q;
     rep->sigma_est = nz.sigma_est;
+    // the next frame's filter variant: decide-before-sweep pays off when the
+    // scan ends by early exit rather than at q_max
+    ctx->hold_guess = ctx->lf_hold >= 0 ? ctx->lf_hold : (h.steps < cfg->q_max);
     rep->masked_fraction = 1.0 - (double)h.included / (double)n;
     rep->criterion_value = h.best_crit;
     const double eps = std::isnan(cfg->epsilon) ? 1e-3 * nz.sigma_est * nz.sigma_est : cfg->epsilon;

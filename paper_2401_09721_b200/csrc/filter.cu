@@ -741,7 +741,7 @@ __device__ __forceinline__ void grid_wait(unsigned int* bar, unsigned int old) {
 }
 
 template <int WM, bool SELECT, int BLK = kBlock, int MINB = 3, bool TMA = false,
-          bool P2P = false, int FAR = 0>
+          bool P2P = false, int FAR = 0, bool HOLD = false>
 __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char dyn_smem[];
@@ -844,12 +844,19 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
       mbar_expect_tx(&s_pbar, bytes);
       bulk_g2s(s_part, a.part + (c & 1) * pstride, bytes, &s_pbar, policy_evict_last());
     }
+    // One more non-improving step would stop the scan (early exit): this
+    // pass only decides step c, and the same iteration then sweeps c+1 --
+    // a stop no longer costs a discarded step.  (s_st is block-uniform.)
+    // (its own instantiation: the check in the loop cost scans that never
+    // early-exit ~0.3 us per step)
+    const bool hold = HOLD && kBulkPart && !decided && s_early && s_st.streak == 2 &&
+                      !(a.fold && c == 1);
     const int ib = s_st.in_b, bb = s_st.best_b;
     int ob = BUF_A;
     if (ob == ib || ob == bb) ob = BUF_B;
     if (ob == ib || ob == bb) ob = BUF_Y;
     TLOG(c, 0);
-    if (c < s_qmax) {
+    if (c < s_qmax && !hold) {
       double sx[3] = {0.0, 0.0, 0.0};
       const bool mask_all = s_mask_all != 0;
       if (TMA) {
@@ -963,6 +970,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_lf_run(StepArgs a) {
     // arrived, so leaving here never strands a waiter)
     if (!SELECT && c >= s_qmax) break;
     if (s_st.stop) break;
+    if (hold) {  // step c decided: sweep c+1 now (nothing written, no barrier)
+      decided = true;
+      continue;
+    }
     if (P2P) {
       // x_{c+1} of every block this one reads (and that reads this one) is
       // published; the acquire orders this block's next loads after it
@@ -1228,9 +1239,9 @@ bool fgbd::lf_contiguous(const fgbd_ctx* ctx, int64_t rows) {
 namespace fgbd {
 
 template <int WM, bool SELECT, int BLK, int MINB, bool TMA = false, bool P2P = false,
-          int FAR = 0>
+          int FAR = 0, bool HOLD = false>
 static int launch_run_k(fgbd_ctx* ctx, StepArgs& a, int slot) {
-  auto kern = k_lf_run<WM, SELECT, BLK, MINB, TMA, P2P, FAR>;
+  auto kern = k_lf_run<WM, SELECT, BLK, MINB, TMA, P2P, FAR, HOLD>;
   constexpr int kEllSmem = (FGBD_LF_ELLSMEM && WM == W_STORED) ? (FGBD_LF_ELLSMEM + 1) * 3 * BLK * 16 : 0;
   const int smem = TMA ? kTmaSmem : kEllSmem;
   if (ctx->coop_blocks[slot] == 0) {
@@ -1330,6 +1341,11 @@ int launch_select_steps_folded(fgbd_ctx* ctx, int64_t n, int q_max, int mode, in
   a.q_max = q_max;
   a.mode = mode;
   a.early_exit = early_exit;
+  // the early-exit variant when this context's last scan stopped early
+  if (ctx->hold_guess && early_exit && ctx->lf_shape == 0)
+    return ctx->lf_far_now
+               ? launch_run_k<W_STORED, true, kBlock, 3, false, false, kFarRows, true>(ctx, a, 49)
+               : launch_run_k<W_STORED, true, kBlock, 3, false, false, 0, true>(ctx, a, 48);
   if (ctx->lf_far_now && ctx->lf_shape == 0)
     return launch_run_k<W_STORED, true, kBlock, 3, false, false, kFarRows>(ctx, a, 45);
   return launch_run<W_STORED, true>(ctx, a);

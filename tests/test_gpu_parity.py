@@ -373,3 +373,27 @@ def test_input_order_matches_oracle(gpu_ready, order):
     assert rep.device["steps"] == ref.steps
     assert rep.sigma_est == pytest.approx(ref.sigma_est, rel=SIGMA_RTOL)
     assert np.max(np.abs(out.colors - ref.colors)) <= COLOR_ATOL
+
+
+# ---------------------------------------------------------------------------
+# the cooperative scan-line front end (csrc/slg.cu) at its boundaries: sizes
+# around a warp / batch / block range, 1-bit to 21-bit codes (one to seven
+# counting passes per line, 32- and 64-bit codes), sorted, reversed and
+# shuffled inputs, duplicate points
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [2, 3, 33, 257, 4097, 70_001])
+@pytest.mark.parametrize("bits", [1, 3, 8, 10, 11, 14, 21])
+def test_slg_front_end_bit_exact(gpu_ready, n, bits):
+    rng = np.random.default_rng(1000 * bits + n)
+    hi = (1 << bits) - 1
+    base = rng.integers(0, hi, size=(n, 3), endpoint=True, dtype=np.int64)
+    base[::7] = base[0]  # duplicate points
+    order = np.lexsort((base[:, 0], base[:, 1], base[:, 2]))
+    for name, coords in (("sorted", base[order]), ("reversed", base[order][::-1]),
+                         ("shuffled", base)):
+        pc = fb.PointCloud(coords, np.zeros((n, 3)), bits)
+        g = fb.build_slg(pc)
+        og = O.build_slg(coords, bits)
+        for key in ("indptr", "indices", "csr_edge", "edge_u", "edge_v"):
+            assert np.array_equal(getattr(g, key), getattr(og, key)), (name, key)
