@@ -618,10 +618,15 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
       return rc;
     frame_colors = ctx->out;
     colors_dev = true;
-  } else if (!dev) {
-    // pageable colours are staged into pinned memory while the coordinates
-    // travel; their DMA then overlaps the graph build
-    frame_colors = static_cast<const double*>(host_prestage(ctx, colors, 3 * n * sizeof(double), 1));
+  } else if (!dev && host_stageable(ctx, colors, 3 * n * sizeof(double))) {
+    // pageable colours: staged right behind the coordinates, each chunk's
+    // DMA (side stream) issued as soon as its copy has landed, so the DMA
+    // overlaps the host copies instead of following them (the colour
+    // expansion on the side stream then reads them on the device)
+    if ((rc = host_to_device(ctx, ctx->out, colors, 3 * n * sizeof(double), ctx->side, 1)))
+      return rc;
+    frame_colors = ctx->out;
+    colors_dev = true;
   }
   bool reuse = false;
   if (trusted) {

@@ -279,10 +279,9 @@ int ensure_capacity(fgbd_ctx* ctx, int64_t n, int key64);
 // DMA issued as soon as it has landed; pinned sources copy directly
 int host_to_device(fgbd_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s,
                    int region);
-// pageable src -> pinned staging region (blocking, parallel); returns the
-// pointer to copy from (src itself when it is pinned or small)
-const void* host_prestage(fgbd_ctx* ctx, const void* src, size_t bytes, int region);
 void destroy_stager(fgbd_ctx* ctx);
+// src is pageable and large enough for the parallel staging above
+bool host_stageable(fgbd_ctx* ctx, const void* src, size_t bytes);
 int require_point_rows(fgbd_ctx* ctx);
 // (N,3) colours (host or device) -> BUF_Y in the (N,4) layout
 int upload_colors(fgbd_ctx* ctx, const double* colors, int64_t n, bool dev);

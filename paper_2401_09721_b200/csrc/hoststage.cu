@@ -159,18 +159,8 @@ int host_to_device(fgbd_ctx* ctx, void* dst, const void* src, size_t bytes, cuda
   return FGBD_OK;
 }
 
-const void* host_prestage(fgbd_ctx* ctx, const void* src, size_t bytes, int region) {
-  int nchunks = 0;
-  char* stage = (bytes && stage_wanted(ctx, src, bytes))
-                    ? stage_begin(ctx, src, bytes, region, &nchunks)
-                    : nullptr;
-  if (!stage) return src;
-  HostStager& h = *ctx->stager;
-  while (stage_step(h)) {
-  }
-  for (int k = 0; k < nchunks; ++k)
-    while (!h.done[k].load(std::memory_order_acquire)) std::this_thread::yield();
-  return stage;
+bool host_stageable(fgbd_ctx* ctx, const void* src, size_t bytes) {
+  return bytes && stage_wanted(ctx, src, bytes);
 }
 
 }  // namespace fgbd
