@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 
 import paper_2401_09721_b200 as fb
-from conftest import cfg_kwargs, custom_input, digest, golden_case, golden_names, regen_input
+from conftest import ROOT, cfg_kwargs, custom_input, digest, golden_case, golden_names, regen_input
 from oracle import fgbd_oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -397,3 +397,40 @@ def test_slg_front_end_bit_exact(gpu_ready, n, bits):
         og = O.build_slg(coords, bits)
         for key in ("indptr", "indices", "csr_edge", "edge_u", "edge_v"):
             assert np.array_equal(getattr(g, key), getattr(og, key)), (name, key)
+
+
+def test_filter_hold_variant_is_bit_identical(gpu_ready, tmp_path):
+    """The decide-before-sweep filter variant (FGBD_LF_HOLD=1; used when a
+    context's last scan stopped early) only reorders work: frames that stop
+    by early exit and by q_max give the same bytes, q, S and trace as the
+    lagged variant (FGBD_LF_HOLD=0).  Separate processes: the knob is read
+    when a context is created."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import hashlib, json, sys, numpy as np\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "import paper_2401_09721_b200 as fb\n"
+        "res = []\n"
+        "for kind, n, sigma in (('two-tone', 200000, 10.0), ('constant', 150000, 10.0),\n"
+        "                       ('ramp', 100000, 10.0)):\n"
+        "    clean, _ = fb.generate_cloud(kind, n, seed=0)\n"
+        "    noisy = fb.add_gaussian_noise(clean, sigma, seed=1)\n"
+        "    for _ in range(2):\n"
+        "        out, rep = fb.denoise(noisy)\n"
+        "        res.append([kind, rep.selected_q, rep.device['steps'],\n"
+        "                    hashlib.sha256(np.ascontiguousarray(out.colors).tobytes()).hexdigest(),\n"
+        "                    rep.device['trace']])\n"
+        "print(json.dumps(res))\n")
+    outs = []
+    for hold in ("0", "1"):
+        env = dict(os.environ, FGBD_LF_HOLD=hold)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
+    assert any(s < 64 for _, _, s, _, _ in outs[0])  # an early exit was exercised
