@@ -821,7 +821,9 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   tl.mark("report");
   if (timing) {
     if (!stages_read) read_stage_times();
-    rep->t_d2h = ev_sec(ev[4], ev[5]);
+    // device outputs have no download (ev4 -> ev5 spans only the control
+    // block's copy): no query after the frame at all
+    rep->t_d2h = dev ? 0.0 : ev_sec(ev[4], ev[5]);
     // the chain ev0 .. ev5, summed (one driver query fewer)
     rep->t_total = rep->t_h2d + rep->t_graph_construction + rep->t_noise_estimation +
                    rep->t_low_pass_filter + rep->t_d2h;
