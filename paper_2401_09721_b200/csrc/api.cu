@@ -467,6 +467,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("FGBD_SORT_DERIVED")) ctx->sort_derived = std::atoi(v);
   if (const char* v = std::getenv("FGBD_SLG_COOP")) ctx->slg_coop = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_ROWS_EXPAND")) ctx->rows_expand = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_HOLD")) ctx->lf_hold = std::atoi(v);
   if (ctx->lf_hold >= 0) ctx->hold_guess = ctx->lf_hold;
   if (const char* v = std::getenv("FGBD_ROWS_GRID")) ctx->rows_grid = std::atoi(v);
@@ -610,6 +611,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   // wait for another context's persistent filter to release the SMs.
   const double* frame_colors = colors;
   bool colors_dev = dev;
+  bool colors_main = dev;  // on the device ahead of the graph build in main-stream order
   if (!dev && !trusted &&
       (rc = host_to_device(ctx, ctx->coords64, coords, 3 * n * sizeof(int64_t), ctx->stream, 0)))
     return rc;
@@ -618,6 +620,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
       return rc;
     frame_colors = ctx->out;
     colors_dev = true;
+    colors_main = true;
   } else if (!dev && host_stageable(ctx, colors, 3 * n * sizeof(double))) {
     // pageable colours: staged right behind the coordinates, each chunk's
     // DMA (side stream) issued as soon as its copy has landed, so the DMA
@@ -629,6 +632,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     colors_dev = true;
   }
   bool reuse = false;
+  bool expanded = false;  // BUF_Y already written by k_rows
   if (trusted) {
     reuse = true;
   } else if (may_reuse) {
@@ -658,16 +662,24 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     ctx->cur_coords = trusted ? ctx->held_coords : frame_coords;
   } else {
     NvtxRange nv("fgbd.graph");
+    // device-resident colours: k_rows lays them out as it walks the rows
+    // (k_expand after k_rows sat on the way to the NE kernel: k_rows fills
+    // the register file, so the two never ran side by side)
+    if (colors_main && ctx->rows_expand) ctx->expand_colors = frame_colors;
     if ((rc = stage_graph(ctx, frame_coords, n, bits, true, w64, !fuse_w, ctx->reorder_rows != 0)))
       return rc;
+    expanded = colors_main && ctx->rows_expand;
+    ctx->expand_colors = nullptr;
     if (want_reuse && (rc = hold_coords(ctx, frame_coords, n))) return rc;
   }
   rep->graph_reused = reuse ? 1 : 0;
   if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[2], ctx->stream));
   tl.mark("graph");
   // colours travel (and are re-laid out) while the graph is being built
-  if ((rc = upload_colors_async(ctx, frame_colors, n, colors_dev))) return rc;
-  FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_side, 0));
+  if (!expanded) {
+    if ((rc = upload_colors_async(ctx, frame_colors, n, colors_dev))) return rc;
+    FGBD_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_side, 0));
+  }
 
   fgbd_noise nz;
   std::memset(&nz, 0, sizeof(nz));

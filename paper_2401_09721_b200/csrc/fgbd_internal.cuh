@@ -193,6 +193,8 @@ struct fgbd_ctx {
   int lf_far_now = 0;           // the choice for the frame being filtered
   int held_far = 0;             // far-slot majority of the held (reused) graph
   int slg_coop = 1;             // FGBD_SLG_COOP: scan-line front end in one cooperative launch
+  const double* expand_colors = nullptr;  // (N,3) device colours k_rows expands into BUF_Y (one build)
+  int rows_expand = 1;          // FGBD_ROWS_EXPAND: device colours expanded by k_rows
   int hold_guess = 0;           // this context's last select-q scan stopped early (early exit)
   int lf_hold = -1;             // FGBD_LF_HOLD: -1 auto (hold_guess), 0 never, 1 always
   int slg_grid[2] = {0, 0};     // its co-resident grid (32- / 64-bit codes)

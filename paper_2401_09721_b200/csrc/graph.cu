@@ -455,7 +455,9 @@ __global__ void __launch_bounds__(kBlock, FGBD_ROWS_MINB) k_rows(const int2* __r
                                                  const uint32_t* __restrict__ rowid, EllRef ell,
                                                  uint32_t* __restrict__ meta,
                                                  double* __restrict__ partials,
-                                                 Ctl* __restrict__ ctl, RowsSlab sl = RowsSlab{}) {
+                                                 Ctl* __restrict__ ctl, RowsSlab sl = RowsSlab{},
+                                                 const double* __restrict__ colors = nullptr,
+                                                 double4* __restrict__ y_rows = nullptr) {
   __shared__ unsigned long long s_red[32 * 2];
   __shared__ bool s_last;
   u128 sg_sum = 0;  // exact: the same bits for any partition of the edges
@@ -470,6 +472,9 @@ __global__ void __launch_bounds__(kBlock, FGBD_ROWS_MINB) k_rows(const int2* __r
   // walk the ROWS (coalesced ELL / meta writes); row rr holds point i
   for (int64_t rr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; rr < n; rr += stride) {
     const int64_t i = rowid ? (int64_t)rowid[rr] : rr;
+    // device-resident colours: k_expand's work for this row rides along
+    if (!SLAB && y_rows)
+      st_row(y_rows + rr, make_double4(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2], 0.0));
     unsigned c[6];
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
@@ -900,6 +905,10 @@ static int run_sort(fgbd_ctx* ctx, int64_t n, int b, int nlines, int passes,
 
 template <typename K>
 static int graph_impl(fgbd_ctx* ctx, int64_t n, int b, bool reorder) {
+  // (N,3) device colours to expand into BUF_Y on the way (fgbd_denoise with
+  // device-resident colours; taken for this build only)
+  const double* colors = ctx->expand_colors;
+  ctx->expand_colors = nullptr;
   int* pos = reorder ? ctx->pos : nullptr;
   if (ctx->slg_coop) {
     // codes, the three orders and the rank neighbours in one launch (slg.cu)
@@ -920,14 +929,15 @@ static int graph_impl(fgbd_ctx* ctx, int64_t n, int b, bool reorder) {
     FGBD_LAUNCH(ctx);
   }
   const int grid = grid_for(n, ctx->rows_grid == 1 ? (1 << 30) : kRowsGrid);
+  double4* y_rows = colors ? reinterpret_cast<double4*>(ctx->buf[BUF_Y]) : nullptr;
   if (b > 15) {
     k_rows<K, true><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b, pos, ctx->rowid,
                                                       EllRef{ctx->nbr, ctx->pay}, ctx->meta, ctx->partials,
-                                                      ctx->ctl);
+                                                      ctx->ctl, RowsSlab{}, colors, y_rows);
   } else {
     k_rows<K, false><<<grid, kBlock, 0, ctx->stream>>>(ctx->cand, (const K*)ctx->pc, n, b, pos, ctx->rowid,
                                                        EllRef{ctx->nbr, ctx->pay}, ctx->meta, ctx->partials,
-                                                       ctx->ctl);
+                                                       ctx->ctl, RowsSlab{}, colors, y_rows);
   }
   FGBD_LAUNCH(ctx);
   return FGBD_OK;
