@@ -434,3 +434,38 @@ def test_filter_hold_variant_is_bit_identical(gpu_ready, tmp_path):
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert outs[0] == outs[1]
     assert any(s < 64 for _, _, s, _, _ in outs[0])  # an early exit was exercised
+
+
+@pytest.mark.parametrize("kind,order", [("ramp", "asis"), ("two-tone", "shuffle"),
+                                        ("constant", "asis"), ("constant", "shuffle")])
+def test_device_pointer_frames_match_host_path(gpu_ready, kind, order):
+    """fgbd_denoise with device-resident inputs and output (the bench's
+    path: colours laid out by k_rows, no host copies) gives the host path's
+    bytes, q, S and trace."""
+    import torch
+
+    from paper_2401_09721_b200 import _native as nat
+
+    clean, _ = fb.generate_cloud(kind, 60_000, seed=0)
+    noisy = fb.add_gaussian_noise(clean, 12.0, seed=3)
+    coords, colors = np.array(noisy.coords), np.array(noisy.colors)
+    if order == "shuffle":
+        perm = np.random.default_rng(9).permutation(coords.shape[0])
+        coords, colors = coords[perm], colors[perm]
+    pc = fb.PointCloud(coords, colors, noisy.bit_depth)
+    out, rep = fb.denoise(pc)
+    ctx = nat.context()
+    dev = torch.device("cuda", 0)
+    d_coords = torch.from_numpy(np.array(coords)).to(dev)
+    d_colors = torch.from_numpy(np.array(colors)).to(dev)
+    d_out = torch.empty_like(d_colors)
+    torch.cuda.synchronize()
+    r = nat.Report()
+    ctx.check(ctx.lib.fgbd_denoise(ctx.handle, d_coords.data_ptr(), d_colors.data_ptr(),
+                                   coords.shape[0], noisy.bit_depth,
+                                   nat.make_config(fb.FilterConfig()), -1, float("nan"),
+                                   d_out.data_ptr(), r, nat.FLAG_DEVICE_PTRS), "denoise")
+    got = d_out.cpu().numpy()
+    assert np.array_equal(got, out.colors)
+    assert (int(r.selected_q), int(r.steps)) == (rep.selected_q, rep.device["steps"])
+    assert [r.trace[k] for k in range(int(r.n_trace))] == rep.device["trace"]
