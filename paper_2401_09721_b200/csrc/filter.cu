@@ -8,16 +8,18 @@
 // k_mask       include_i = !(eligible_i && stat_i > 2 sigma_est), packed to
 //              1 bit/point by warp ballot; sums count and sum_inc y^2; its
 //              last block initialises the select_q state (q = 0).
-// k_lf_persist the whole q scan in ONE cooperative launch: every block owns
-//              a fixed set of rows; per step it applies
+// k_lf_run     the whole q scan in ONE cooperative launch (persistent, 3
+//              blocks of 256 per SM): per step every row applies
 //              out = (d f + sum_j w_ij f_j) / (2 d) in the reference's exact
 //              arithmetic order (slot-order accumulation from 0.0, no FMA,
-//              d = sum_{j>i} w + sum_{j<i} w), adds its rows' masked out^2 to
-//              a block partial, and after grid.sync() every block reduces
-//              the partials in the same fixed order, evaluates Eq. (6) and
-//              runs select_q's bookkeeping (strict improvement, 3-rise early
-//              exit, best_crit == 0 stop) identically -- no host round trip,
-//              no launch per step, no empty launches after early exit.
+//              d = sum_{j>i} w + sum_{j<i} w) and adds its masked out^2 to a
+//              block partial; the select_q decision for step q-1 (Eq. (6),
+//              strict improvement, 3-rise early exit, best_crit == 0 stop)
+//              is taken by every block from bulk-copied partials while step
+//              q sweeps (lagged by one step), or before it when one more
+//              rise would stop the scan (HOLD).  On the denoise path step 1
+//              also builds the FSLR mask and select_q's initial totals
+//              (k_mask's work, fold).  No host round trip, one launch.
 // k_lf_step    one step per launch (variant 0, kept for comparison).
 // k_compact    (N,4) -> (N,3), optionally clipped to [0, 255] (filtering.py:327).
 #include <cooperative_groups.h>
