@@ -1,5 +1,10 @@
 // Scan-line graph construction on sm_100a (reference graph.py:122-251).
 //
+// The denoise path builds the three scan-line orders and the rank
+// neighbours in one cooperative launch (slg.cu, k_slg) and then runs k_rows
+// below.  The kernels before k_rows here (k_prep, k_onesweep, k_neighbors)
+// serve the argsort / scan-line stage entry points and FGBD_SLG_COOP=0.
+//
 //   k_prep       coords int64 -> packed line-1 code (pc) + digit histograms
 //                of every radix pass (one read); flags an input that is not
 //                already in scan-line-1 order
