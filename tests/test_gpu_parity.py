@@ -469,3 +469,39 @@ def test_device_pointer_frames_match_host_path(gpu_ready, kind, order):
     assert np.array_equal(got, out.colors)
     assert (int(r.selected_q), int(r.steps)) == (rep.selected_q, rep.device["steps"])
     assert [r.trace[k] for k in range(int(r.n_trace))] == rep.device["trace"]
+
+
+def test_no_timing_frames_match(gpu_ready):
+    """FGBD_FLAG_NO_TIMING (no stage events; the frame's waits take the
+    other branches) gives the same bytes and q for device and host buffers,
+    with zero stage times."""
+    import torch
+
+    from paper_2401_09721_b200 import _native as nat
+
+    clean, _ = fb.generate_cloud("two-tone", 50_000, seed=0)
+    noisy = fb.add_gaussian_noise(clean, 12.0, seed=4)
+    out, rep = fb.denoise(noisy)
+    ctx = nat.context()
+    cfg = nat.make_config(fb.FilterConfig())
+    n = noisy.n_points
+    # device buffers
+    d_coords = torch.from_numpy(np.array(noisy.coords)).cuda()
+    d_colors = torch.from_numpy(np.array(noisy.colors)).cuda()
+    d_out = torch.empty_like(d_colors)
+    torch.cuda.synchronize()
+    r = nat.Report()
+    ctx.check(ctx.lib.fgbd_denoise(ctx.handle, d_coords.data_ptr(), d_colors.data_ptr(), n,
+                                   noisy.bit_depth, cfg, -1, float("nan"), d_out.data_ptr(), r,
+                                   nat.FLAG_DEVICE_PTRS | nat.FLAG_NO_TIMING), "denoise")
+    assert np.array_equal(d_out.cpu().numpy(), out.colors)
+    assert int(r.selected_q) == rep.selected_q and r.t_total == 0.0
+    # host buffers
+    h_out = np.empty((n, 3), np.float64)
+    r2 = nat.Report()
+    ctx.check(ctx.lib.fgbd_denoise(ctx.handle, nat.ptr(np.ascontiguousarray(noisy.coords)),
+                                   nat.ptr(np.ascontiguousarray(noisy.colors)), n,
+                                   noisy.bit_depth, cfg, -1, float("nan"), nat.ptr(h_out), r2,
+                                   nat.FLAG_NO_TIMING), "denoise")
+    assert np.array_equal(h_out, out.colors)
+    assert int(r2.selected_q) == rep.selected_q and r2.t_total == 0.0
