@@ -316,7 +316,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // arrives), a RELAXED spin, then one acquire fence.  cooperative_groups'
 // grid.sync() spins with acquire loads, i.e. an L1 invalidation (CCTL.IVALL)
 // per poll, which keeps wiping the L1 of the blocks on the same SM that are
-// still working; here each block invalidates once, on leaving.
+// still working; here each block invalidates once, on leaving.  Measured
+// (tools/micro/gridbar.cu, no work between barriers): 1.26 / 1.42 / 1.80 us
+// per barrier at 148 / 296 / 444 blocks, against 1.2 us for grid.sync() at
+// any of those sizes.  Inside kernels that move data the order flips:
+// k_slg with grid.sync() spent ~1 us more per scan phase (B + barrier 4.2 vs
+// 3.3 us at 1M), so it keeps this one; k_lf_run keeps grid.sync()
+// (FGBD_LF_BAR).
 __device__ __forceinline__ void grid_barrier(unsigned int* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
