@@ -633,6 +633,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   }
   bool reuse = false;
   bool expanded = false;  // BUF_Y already written by k_rows
+  std::unique_lock<std::mutex> compute_lock(device_mutex(ctx->device), std::defer_lock);
   if (trusted) {
     reuse = true;
   } else if (may_reuse) {
@@ -640,9 +641,13 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = coords_equal(ctx, frame_coords, ctx->held_coords, 3 * n, &same))) return rc;
     reuse = same != 0;
   } else if (!dev) {
-    FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    // The coordinates are uploading.  A free device: queue the frame behind
+    // them at once (stream order; the host waiting first left the GPU idle
+    // ~19 us while it enqueued the graph).  A busy one: let them land before
+    // queuing for it, so another context's compute overlaps this upload.
+    if (!compute_lock.try_lock()) FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   }
-  std::unique_lock<std::mutex> compute_lock(device_mutex(ctx->device));
+  if (!compute_lock.owns_lock()) compute_lock.lock();
   // the side stream starts after the coordinates have landed (full PCIe
   // bandwidth for them) and after all earlier main-stream work on the
   // staging buffers; it then overlaps the colour upload with the graph build
