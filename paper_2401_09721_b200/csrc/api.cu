@@ -766,8 +766,13 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   // a frame with a host round trip inside keeps the lock until it is done
   const bool held = !ctx->async_lock || (cached_q < 0 && !device_ne);
   // device outputs: nothing follows, so the frame's last event goes in now
-  // (recording it after the wait cost a submission round trip, ~10 us)
-  if (dev && timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
+  // (recording it after the wait cost a submission round trip, ~10 us);
+  // host outputs: the download too, right behind the compute -- enqueued
+  // after the wait it started a host wake-up late.  It is outside the
+  // compute order (ev_done), so other contexts' frames never wait for it.
+  NvtxRange nv_out("fgbd.download");
+  if (!dev && (rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), false))) return rc;
+  if (timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
   tl.mark("enqueued");
   // Each elapsed-time query is a ~3.5 us driver call: a frame that waits
   // here anyway reads the stage times while the filter still runs, so only
@@ -793,9 +798,6 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
   }
   tl.mark("done");
   compute_lock.unlock();
-  NvtxRange nv_out("fgbd.download");
-  if (!dev && (rc = d2h(ctx, out_colors, ctx->out, 3 * n * sizeof(double), false))) return rc;
-  if (!dev && timing) FGBD_CUDA(ctx, cudaEventRecord(ev[5], ctx->stream));
   if (!dev || !held) FGBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   tl.mark("synced");
   if ((rc = check_graph_ctl(ctx, bits))) return rc;
