@@ -467,6 +467,7 @@ fgbd_ctx* fgbd_ctx_create(int32_t device, int64_t max_points) {
   if (const char* v = std::getenv("FGBD_PREP_MULT")) ctx->prep_mult = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("FGBD_SORT_DERIVED")) ctx->sort_derived = std::atoi(v);
   if (const char* v = std::getenv("FGBD_SLG_COOP")) ctx->slg_coop = std::atoi(v);
+  if (const char* v = std::getenv("FGBD_JACOBI_THREADS")) ctx->jacobi_threads = std::atoi(v);
   if (const char* v = std::getenv("FGBD_ROWS_EXPAND")) ctx->rows_expand = std::atoi(v);
   if (const char* v = std::getenv("FGBD_LF_HOLD")) ctx->lf_hold = std::atoi(v);
   if (ctx->lf_hold >= 0) ctx->hold_guess = ctx->lf_hold;
@@ -723,6 +724,7 @@ int32_t fgbd_denoise(fgbd_ctx* ctx, const int64_t* coords, const double* colors,
     if ((rc = launch_compact(ctx, n, -1, dev ? out_colors : ctx->out, 1))) return rc;
   } else if (cached_q < 0) {
     const int D = cfg->patch_size;
+    if (ctx->jacobi_threads) jacobi_pool_prepare();  // helpers spin while NE runs
     tl.mark("ne_launched");
     if ((rc = pull_ctl(ctx))) return rc;
     tl.mark("ne_pulled");

@@ -193,6 +193,7 @@ struct fgbd_ctx {
   int lf_far_now = 0;           // the choice for the frame being filtered
   int held_far = 0;             // far-slot majority of the held (reused) graph
   int slg_coop = 1;             // FGBD_SLG_COOP: scan-line front end in one cooperative launch
+  int jacobi_threads = 1;       // FGBD_JACOBI_THREADS: the 3 channels on 3 host threads
   const double* expand_colors = nullptr;  // (N,3) device colours k_rows expands into BUF_Y (one build)
   int rows_expand = 1;          // FGBD_ROWS_EXPAND: device colours expanded by k_rows
   int hold_guess = 0;           // this context's last select-q scan stopped early (early exit)
@@ -338,6 +339,8 @@ int jacobi_eigenvalues(const double* s, int d, double* out_desc, std::string* er
                        int* direct_off);
 int jacobi_eigenvalues_multi(int nm, const double* const* s, int d, double* const* out_desc,
                              std::string* err, int* rc, int* direct_off);
+// wake the Jacobi helper threads (finish_noise follows within ~2 ms)
+void jacobi_pool_prepare();
 int select_tail_host(const double* lam, int d, int divisor, int* m, double* tau,
                      int* fallback, std::string* err);
 

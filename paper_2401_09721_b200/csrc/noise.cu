@@ -18,6 +18,11 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 
 #include "device_util.cuh"
 #include "fgbd_internal.cuh"
@@ -976,6 +981,102 @@ int collect_noise(fgbd_ctx* ctx, int D, fgbd_noise* out) {
 
 // Reads the reduced moments (ctl mirror must be current) and finishes
 // noise.py:122-243 on the host.
+// Three channels' Jacobi on three host threads.  Two helper threads per
+// process are woken while the NE kernels run (jacobi_pool_prepare) and spin
+// for the job; channels are claimed through one counter, so a helper that
+// has gone back to sleep (a long wait) is simply not needed -- the calling
+// thread claims what is left.  Each channel's arithmetic is
+// jacobi_eigenvalues', so the result is bit-identical to the sequential
+// and lockstep versions.
+namespace {
+struct JacobiPool {
+  std::mutex m;
+  std::condition_variable cv;
+  unsigned wake = 0;                 // generation of prepare() calls (under m)
+  std::atomic<unsigned> job{0};      // generation of posted jobs
+  std::atomic<int> next{0}, done{0};
+  std::atomic<bool> busy{false};
+  const double* const* s = nullptr;
+  double* const* out = nullptr;
+  std::string* err = nullptr;
+  int* rc = nullptr;
+  int* direct = nullptr;
+  int d = 0;
+  std::thread th[2];
+
+  JacobiPool() {
+    for (auto& t : th) {
+      t = std::thread([this] { loop(); });
+      t.detach();  // process lifetime
+    }
+  }
+  void run_claimed() {
+    for (int c; (c = next.fetch_add(1)) < 3;) {
+      jacobi_eigenvalues_multi(1, s + c, d, out + c, err + c, rc + c, direct + c);
+      done.fetch_add(1, std::memory_order_release);
+    }
+  }
+  void loop() {
+    unsigned seen_wake = 0, seen_job = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(m);
+        cv.wait(lk, [&] { return wake != seen_wake; });
+        seen_wake = wake;
+      }
+      const auto t0 = std::chrono::steady_clock::now();
+      for (;;) {  // spin for the job: the NE kernels are about to finish
+        const unsigned j = job.load(std::memory_order_acquire);
+        if (j != seen_job) {
+          seen_job = j;
+          run_claimed();
+          break;
+        }
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) break;
+      }
+    }
+  }
+};
+JacobiPool& jacobi_pool() {
+  static JacobiPool* p = new JacobiPool();  // never destroyed: detached helpers
+  return *p;
+}
+}  // namespace
+
+void jacobi_pool_prepare() {
+  JacobiPool& p = jacobi_pool();
+  // try_lock: a helper holds m only on its way into the wait; if the wake is
+  // skipped, the calling thread just computes the channels itself (also
+  // after a fork, where the helpers do not exist)
+  std::unique_lock<std::mutex> lk(p.m, std::try_to_lock);
+  if (!lk.owns_lock()) return;
+  ++p.wake;
+  lk.unlock();
+  p.cv.notify_all();
+}
+
+static void jacobi_three(const double* const* s, int d, double* const* out, std::string* err,
+                         int* rc, int* direct) {
+  JacobiPool& p = jacobi_pool();
+  if (p.busy.exchange(true, std::memory_order_acquire)) {  // another context's frame
+    jacobi_eigenvalues_multi(3, s, d, out, err, rc, direct);
+    return;
+  }
+  p.s = s;
+  p.out = out;
+  p.err = err;
+  p.rc = rc;
+  p.direct = direct;
+  p.d = d;
+  p.done.store(0, std::memory_order_relaxed);
+  p.next.store(0, std::memory_order_relaxed);
+  p.job.fetch_add(1, std::memory_order_release);
+  p.run_claimed();
+  while (p.done.load(std::memory_order_acquire) < 3) {
+  }
+  p.busy.store(false, std::memory_order_release);
+}
+
 int finish_noise(fgbd_ctx* ctx, int D, int divisor, fgbd_noise* out) {
   const Ctl& h = *ctx->ctl_host;
   std::memset(out, 0, sizeof(*out));
@@ -1009,7 +1110,8 @@ int finish_noise(fgbd_ctx* ctx, int D, int divisor, fgbd_noise* out) {
   {
     const double* sm[3] = {cov[0], cov[1], cov[2]};
     double* om[3] = {lam[0], lam[1], lam[2]};
-    jacobi_eigenvalues_multi(3, sm, D, om, jerr, jrc, out->jacobi_direct_off);
+    if (ctx->jacobi_threads) jacobi_three(sm, D, om, jerr, jrc, out->jacobi_direct_off);
+    else jacobi_eigenvalues_multi(3, sm, D, om, jerr, jrc, out->jacobi_direct_off);
   }
   for (int c = 0; c < 3; ++c) {
     std::string err;
